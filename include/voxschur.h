@@ -1,0 +1,131 @@
+/*
+ * voxschur.h -- C ABI of the B200-native pressure-Schur-complement Stokes path.
+ *
+ * Drop-in boundary for the reference package `voxstokes`
+ * (/root/reference/pkg/src/voxstokes).  The reference is pure Python, so the
+ * binding a maintainer adds is a ctypes stub; the Python
+ * mirror of the reference API in paper_2307_05266_b200/ is that stub.
+ *
+ * Conventions
+ *   - every function returns an int status: VS_OK, VS_EVALUE (the reference
+ *     raises ValueError), VS_ERUNTIME (the reference raises RuntimeError),
+ *     VS_ECUDA (device/internal failure).  On failure the message is written
+ *     to the thread-local buffer returned by vs_last_error(); messages for
+ *     VS_EVALUE / VS_ERUNTIME are byte-identical to the reference's.
+ *   - host pointers in, host pointers out (caller owns them); the library
+ *     owns all device memory inside an opaque context.  No callbacks.
+ *   - vectors use the reference DOF order: velocity axis-major, then C-order
+ *     of the face position (last axis fastest); pressure C-order over fluid
+ *     voxels (operators.py:239-249).
+ *   - one context = one device + one CUDA stream; contexts are independent
+ *     and may be used from different threads.
+ */
+#ifndef VOXSCHUR_H
+#define VOXSCHUR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VS_OK 0
+#define VS_EVALUE 1
+#define VS_ERUNTIME 2
+#define VS_ECUDA 3
+
+typedef struct vs_ctx vs_ctx;
+
+/* Scalars of one Schur solve (schur.py:113-136 SolveReport, minus arrays). */
+typedef struct {
+    double k_value;              /* permeability of the refreshed velocity  */
+    int64_t iters_outer;
+    int32_t converged;
+    int32_t _pad;
+    int64_t inner_velocity;      /* inner_iter_totals["velocity"]           */
+    int64_t inner_preconditioner;/* inner_iter_totals["preconditioner"]     */
+    int64_t uf_iters;            /* discarded u_f solve count (schur.py:230) */
+    int64_t n_hist;              /* entries written to each history array   */
+    double device_ms;            /* CUDA-event time of the device solve     */
+} vs_report;
+
+/* Solve settings (schur.py:64-75 SchurConfig) + host-computed constants. */
+typedef struct {
+    int32_t prec;                /* 0 = uzawa, 1 = simple                   */
+    int32_t outer_norm;          /* 0 = preconditioned, 1 = unpreconditioned*/
+    double eps_S, eps_A, eps_Shat;
+    int64_t max_iter;
+    double h_pow_dim;            /* h**dim as Python computes it (schur.py:288) */
+} vs_schur_cfg;
+
+/* Thread-local message of the last failing call. */
+const char *vs_last_error(void);
+
+/* Library build string (arch, version). */
+const char *vs_version(void);
+
+/* Periodic face-adjacency components of a mask (geometry.py:183-222).
+ * labels (nullable) receives ids in first row-major appearance, -1 on solid. */
+int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels,
+                  int64_t *n_components);
+
+/* assemble() (operators.py:209-302): validation, connectivity check, and
+ * the on-device geometry build (face masks, DOF ranks, diag codes).
+ * inv_h = 1.0/h and inv_h2 = 1.0/h**2 as the reference computes them
+ * (operators.py:107-108); the diagonal scale (n/1.0)**2 is exact. */
+int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir,
+                  int check_connectivity, int require_walls, int device,
+                  double inv_h, double inv_h2, vs_ctx **out);
+void vs_ctx_destroy(vs_ctx *ctx);
+
+/* DofMap sizes (operators.py:233-235, :247). */
+int vs_counts(vs_ctx *ctx, int64_t *m_u, int64_t *m_p, int64_t axis_counts[3]);
+
+/* Geometry export for parity tests: per-component face masks and the
+ * pressure mask as n^dim uint8 grids (nullable), and the integer no-slip
+ * diagonal code of every velocity DOF (laplacian_diag = code * n^2). */
+int vs_export_geometry(vs_ctx *ctx, uint8_t *face_mask0, uint8_t *face_mask1,
+                       uint8_t *face_mask2, uint8_t *pressure_mask,
+                       uint8_t *diag_code);
+
+/* Single operator applies, bitwise equal to the reference. */
+int vs_apply_laplacian(vs_ctx *ctx, const double *u, double *out);   /* operators.py:131 */
+int vs_apply_divergence(vs_ctx *ctx, const double *u, double *out);  /* operators.py:137 */
+int vs_apply_gradient(vs_ctx *ctx, const double *p, double *out);    /* operators.py:146 */
+int vs_divergence_weighted_diagonal(vs_ctx *ctx, const double *w, double *out); /* :194 */
+int vs_apply_simple(vs_ctx *ctx, const double *p, double *out);      /* schur.py:234 */
+
+/* Inner solves (schur.py:200-219, :243-272): fused device PCG.
+ * x0 nullable (zeros).  *iters receives the iteration count. */
+int vs_solve_velocity(vs_ctx *ctx, const double *rhs, const double *x0,
+                      double eps, double *x, int64_t *iters);
+int vs_solve_simple(vs_ctx *ctx, const double *r, double eps, double *z,
+                    int64_t *iters);
+
+/* solve_schur (schur.py:291-385).  pressure/velocity nullable (stay on the
+ * device).  History arrays (nullable) need capacity max_iter+1; alpha/beta
+ * capacity max_iter. */
+int vs_solve_schur(vs_ctx *ctx, const vs_schur_cfg *cfg, double *pressure,
+                   double *velocity, vs_report *rep, double *res_prec,
+                   double *res_unprec, double *perm_history, double *alpha,
+                   double *beta);
+
+/* Bench hooks: CUDA-event timing of the fused persistent CG launches of the
+ * most recent vs_solve_schur / inner solve, split by operator.  dof_iters =
+ * sum over launches of (iterations x vector length); launches counts kernel
+ * launches of the library in that call (all kernels, not only CG). */
+typedef struct {
+    int64_t launches;     /* persistent CG launches for this operator   */
+    int64_t iterations;   /* CG iterations summed over those launches   */
+    int64_t dof_iters;    /* iterations x DOFs summed over launches     */
+    double ms;            /* summed CUDA-event duration of the launches */
+} vs_kstat;
+
+int vs_kernel_stats(vs_ctx *ctx, vs_kstat *velocity_cg, vs_kstat *simple_cg,
+                    int64_t *total_kernel_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOXSCHUR_H */

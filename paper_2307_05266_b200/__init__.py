@@ -1,0 +1,32 @@
+"""B200-native drop-in for the `voxstokes` Schur-complement Stokes path.
+
+Same public names as the reference package for the hot path
+(geometry input type, assemble, the Krylov seam, the Schur driver);
+every apply and solve runs in libvoxschur.so (sm_100a CUDA).
+"""
+from .geometry import VoxelGrid, connected_components, enforce_connectivity
+from .krylov import PcgConfig, PcgResult, jacobi_prec, lanczos_condition_estimate, pcg
+from .operators import DofMap, StaggeredSystem, assemble, axis_index
+from .schur import (
+    TOLERANCE_PROFILES,
+    SchurConfig,
+    SolveReport,
+    apply_schur,
+    apply_simple_inverse,
+    last_kernel_stats,
+    permeability,
+    profile_config,
+    schur_rhs,
+    solve_schur,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "VoxelGrid", "connected_components", "enforce_connectivity",
+    "PcgConfig", "PcgResult", "jacobi_prec", "lanczos_condition_estimate", "pcg",
+    "DofMap", "StaggeredSystem", "assemble", "axis_index",
+    "TOLERANCE_PROFILES", "SchurConfig", "SolveReport", "apply_schur", "apply_simple_inverse",
+    "last_kernel_stats", "permeability", "profile_config", "schur_rhs", "solve_schur",
+    "__version__",
+]

@@ -1,0 +1,69 @@
+// vs_internal.h -- host-side declarations shared by the API and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vs_device.cuh"
+
+namespace vs {
+
+constexpr int CG_THREADS = 256;
+constexpr int RED_THREADS = 256;
+constexpr int RED_MAX_BLOCKS = 592;
+
+struct CgOut {
+    int64_t iterations;
+    int32_t converged;
+    int32_t status;  // 0 ok, 1 r'z < 0, 2 d'q <= 0, 3 non-finite
+    double value;
+    int64_t at_iter;
+    double res_prec0, res_unprec0, res_prec_last, res_unprec_last;
+};
+
+struct CgParams {
+    Geo g;
+    int64_t m;
+    const uint64_t *rec;
+    const double *rhs, *x0;
+    double *x, *r, *d0, *d1;
+    double *part;  // 4 sets x 8 slots x grid
+    CgOut *out;
+    double tol;
+    int64_t max_iter;
+    int norm_prec;
+    double inv_h, inv_h2;
+    double diag_code[16];
+    double inv_code[16];
+    double invA_enc[8];
+    const double *invS;
+};
+
+void launch_pack_fluid(const uint8_t *fluid, const Geo &g, int64_t nwords, uint32_t *fbits, cudaStream_t s);
+void launch_face_bits(const Geo &g, int a, int64_t nwords, uint32_t *out, cudaStream_t s);
+cudaError_t build_meta(const uint32_t *bits, int64_t nwords, uint32_t off, uint2 *meta, uint32_t *scratch_cnt,
+                       uint32_t *scratch_base, void *temp, size_t temp_bytes, cudaStream_t s);
+size_t scan_temp_bytes(int64_t nwords);
+void launch_vel_records(const Geo &g, int a, int64_t nwords, uint64_t *rec, cudaStream_t s);
+void launch_p_records(const Geo &g, int64_t nwords, uint64_t *rec, cudaStream_t s);
+void launch_bits_to_u8(const uint2 *meta, const uint32_t *bits, const Geo &g, int64_t ncells, uint8_t *out,
+                       cudaStream_t s);
+void launch_vcodes(const uint64_t *rec, int64_t m, uint8_t *out, cudaStream_t s);
+void launch_zero_sdiag(const uint64_t *prec, int64_t m, int *flag, cudaStream_t s);
+void launch_apply_A(const Geo &g, const uint64_t *rec, const double *u, double *out, int64_t m,
+                    const double *diag_code, double inv_h2, cudaStream_t s);
+void launch_apply_div(const Geo &g, const uint64_t *prec, const double *u, double *out, int64_t m, double inv_h,
+                      cudaStream_t s);
+void launch_apply_grad(const Geo &g, const uint64_t *vrec, const double *p, double *out, int64_t m,
+                       double inv_h, cudaStream_t s);
+void launch_apply_S(const Geo &g, const uint64_t *prec, const double *p, double *out, int64_t m,
+                    const double *invA_enc, double inv_h, cudaStream_t s);
+void launch_dwd(const Geo &g, const uint64_t *prec, const double *w, double *out, int64_t m, double inv_h2,
+                cudaStream_t s);
+void launch_vec(int kind, double *out, double *a, const double *b, double sc, int64_t m, cudaStream_t s);
+void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s);
+int launch_reduce(int kind, const double *a, const double *b, int64_t m, double *part, double *out,
+                  cudaStream_t s);
+int pcg_max_grid(int op, int proj, int device);
+cudaError_t launch_pcg(int op, int proj, CgParams &P, int grid, cudaStream_t s);
+
+}  // namespace vs

@@ -1,0 +1,541 @@
+// vs_kernels.cu -- sm_100a kernels of the Schur-complement Stokes path.
+//
+//   K1  geometry build   (operators.py:232-297)  integer, bit-exact
+//   K2-K6 operator applies (operators.py:131-206, schur.py:234-240) bit-exact
+//   K8  fused persistent PCG (krylov.py:76-182) for A and S_hat: two passes
+//       per iteration, device-resident scalars, deterministic grid reductions
+//   outer-loop vector kernels + deterministic reductions (schur.py:291-385)
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+
+#include "vs_device.cuh"
+#include "vs_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace vs {
+
+// ------------------------------------------------------------ K1 geometry
+
+__device__ __forceinline__ Cell word_cell(const Geo &g, int64_t word, int b) {
+    const int L = (int)(word / g.nw);
+    const int w = (int)(word % g.nw);
+    Cell c;
+    if (g.dim == 3) { c.x = L / g.n; c.y = L % g.n; } else { c.x = L; c.y = 0; }
+    c.z = w * 32 + b;
+    return c;
+}
+
+__global__ void k_pack_fluid(const uint8_t *fluid, Geo g, int64_t nwords, uint32_t *fbits) {
+    const int64_t word = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (word >= nwords) return;
+    const int64_t L = word / g.nw;
+    const int w = (int)(word % g.nw);
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int z = w * 32 + b;
+        if (z < g.n && fluid[L * g.n + z]) bits |= 1u << b;
+    }
+    fbits[word] = bits;
+}
+
+// face (a, I) carries a DOF iff fluid[I] && fluid[I - e_a]  (operators.py:232)
+__global__ void k_face_bits(Geo g, int a, int64_t nwords, uint32_t *out) {
+    const int64_t word = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (word >= nwords) return;
+    const int ia = iaxis(g.dim, a);
+    uint32_t fb = g.fbits[word], bits = 0;
+    while (fb) {
+        const int b = __ffs(fb) - 1;
+        fb &= fb - 1;
+        const Cell c = word_cell(g, word, b);
+        if (fluid_at(g, shifted(c, ia, -1, g.n))) bits |= 1u << b;
+    }
+    out[word] = bits;
+}
+
+__global__ void k_popc(const uint32_t *bits, int64_t nwords, uint32_t *cnt) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < nwords) cnt[i] = __popc(bits[i]);
+}
+
+__global__ void k_make_meta(const uint32_t *bits, const uint32_t *base, uint32_t off,
+                            int64_t nwords, uint2 *meta) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < nwords) meta[i] = make_uint2(bits[i], base[i] + off);
+}
+
+// integer no-slip code of the existing face (a, c) (operators.py:268-281)
+__device__ int face_code(const Geo &g, int a, Cell c) {
+    const int ia = iaxis(g.dim, a);
+    int code = 0;
+    for (int d = 0; d < g.dim; ++d) {
+        const int id = iaxis(g.dim, d);
+        for (int si = 0; si < 2; ++si) {
+            if (d == a) { code += 1; continue; }
+            const Cell cn = shifted(c, id, si == 0 ? 1 : -1, g.n);
+            const bool hi = fluid_at(g, cn);
+            const bool lo = fluid_at(g, shifted(cn, ia, -1, g.n));
+            const bool nb_face = hi && lo;
+            code += (!nb_face && !hi && !lo) ? 2 : 1;
+        }
+    }
+    return code;
+}
+
+__global__ void k_vel_records(Geo g, int a, int64_t nwords, uint64_t *rec) {
+    const int64_t word = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (word >= nwords) return;
+    const uint2 m = g.vmeta[a][word];
+    uint32_t bits = m.x, k = 0;
+    while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const Cell c = word_cell(g, word, b);
+        const int code = face_code(g, a, c);
+        rec[m.y + k] = make_rec(c.x, c.y, c.z, a) | ((uint64_t)code << 36);
+        ++k;
+    }
+}
+
+__global__ void k_p_records(Geo g, int64_t nwords, uint64_t *rec) {
+    const int64_t word = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (word >= nwords) return;
+    const uint2 m = g.pmeta[word];
+    const int cbase = 2 * g.dim - 1;
+    uint32_t bits = m.x, k = 0;
+    while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const Cell c = word_cell(g, word, b);
+        uint64_t r = make_rec(c.x, c.y, c.z, 0);
+        for (int a = 0; a < g.dim; ++a) {
+            const int ia = iaxis(g.dim, a);
+            if (fluid_at(g, shifted(c, ia, -1, g.n)))
+                r |= (uint64_t)(face_code(g, a, c) - cbase) << (40 + 3 * a);
+            const Cell cp = shifted(c, ia, 1, g.n);
+            if (fluid_at(g, cp))
+                r |= (uint64_t)(face_code(g, a, cp) - cbase) << (49 + 3 * a);
+        }
+        rec[m.y + k] = r;
+        ++k;
+    }
+}
+
+__global__ void k_bits_to_u8(const uint2 *meta, const uint32_t *bits_plain, Geo g, int64_t ncells,
+                             uint8_t *out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= ncells) return;
+    const int64_t L = i / g.n;
+    const int z = (int)(i % g.n);
+    const uint32_t w = meta ? meta[L * g.nw + (z >> 5)].x : bits_plain[L * g.nw + (z >> 5)];
+    out[i] = (w >> (z & 31)) & 1u;
+}
+
+__global__ void k_vcodes(const uint64_t *rec, int64_t m, uint8_t *out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m) out[i] = (uint8_t)rec_vcode(rec[i]);
+}
+
+// any fluid cell with no velocity face at all -> diag(S_hat) == 0
+__global__ void k_zero_sdiag(const uint64_t *prec, int64_t m, int *flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < m && rec_pkey(prec[i]) == 0) atomicOr(flag, 1);
+}
+
+// --------------------------------------------------------- operator applies
+
+__global__ void k_apply_A(Geo g, const uint64_t *rec, const double *u, double *out, int64_t m,
+                          const double *diag_code, double inv_h2) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint64_t r = rec[i];
+    out[i] = apply_A_at(g, r, u[i], diag_code[rec_vcode(r)], inv_h2,
+                        [&](uint32_t j) { return u[j]; });
+}
+
+// B (operators.py:137-144): out = 0; out += u_in - u_out per axis; * inv_h
+__global__ void k_apply_div(Geo g, const uint64_t *prec, const double *u, double *out, int64_t m,
+                            double inv_h) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint64_t r = prec[i];
+    const Cell c = rec_cell(r);
+    double acc = 0.0;
+    for (int a = 0; a < g.dim; ++a) {
+        const double vin = rec_pin(r, a) ? u[rank_at(g.vmeta[a], g, c)] : 0.0;
+        const double vout =
+            rec_pout(r, a) ? u[rank_at(g.vmeta[a], g, shifted(c, iaxis(g.dim, a), 1, g.n))] : 0.0;
+        acc = __dadd_rn(acc, __dsub_rn(vin, vout));
+    }
+    out[i] = __dmul_rn(acc, inv_h);
+}
+
+// B^T (operators.py:146-153): (p[I] - p[I - e_a]) * inv_h
+__global__ void k_apply_grad(Geo g, const uint64_t *vrec, const double *p, double *out, int64_t m,
+                             double inv_h) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint64_t r = vrec[i];
+    const Cell c = rec_cell(r);
+    const int a = rec_comp(r);
+    const double hi = p[rank_at(g.pmeta, g, c)];
+    const double lo = p[rank_at(g.pmeta, g, shifted(c, iaxis(g.dim, a), -1, g.n))];
+    out[i] = __dmul_rn(__dsub_rn(hi, lo), inv_h);
+}
+
+__global__ void k_apply_S(Geo g, const uint64_t *prec, const double *p, double *out, int64_t m,
+                          const double *invA_enc, double inv_h) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    out[i] = apply_S_at(g, prec[i], p[i], invA_enc, inv_h, [&](uint32_t j) { return p[j]; });
+}
+
+// diag(B W B^T) (operators.py:194-206): out += w_in + w_out; * inv_h2
+__global__ void k_dwd(Geo g, const uint64_t *prec, const double *w, double *out, int64_t m,
+                      double inv_h2) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint64_t r = prec[i];
+    const Cell c = rec_cell(r);
+    double acc = 0.0;
+    for (int a = 0; a < g.dim; ++a) {
+        const double vin = rec_pin(r, a) ? w[rank_at(g.vmeta[a], g, c)] : 0.0;
+        const double vout =
+            rec_pout(r, a) ? w[rank_at(g.vmeta[a], g, shifted(c, iaxis(g.dim, a), 1, g.n))] : 0.0;
+        acc = __dadd_rn(acc, __dadd_rn(vin, vout));
+    }
+    out[i] = __dmul_rn(acc, inv_h2);
+}
+
+// ------------------------------------------------------ outer vector ops
+
+// kind: 0 out=a-s ; 1 a-=s*b ; 2 a+=s*b ; 3 out=b+s*a (d = z + beta d) ; 4 out=a-b
+__global__ void k_vec(int kind, double *out, double *a, const double *b, double s, int64_t m) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    switch (kind) {
+        case 0: out[i] = __dsub_rn(a[i], s); break;
+        case 1: a[i] = __dsub_rn(a[i], __dmul_rn(s, b[i])); break;
+        case 2: a[i] = __dadd_rn(a[i], __dmul_rn(s, b[i])); break;
+        case 3: out[i] = __dadd_rn(b[i], __dmul_rn(s, a[i])); break;
+        case 4: out[i] = __dsub_rn(a[i], b[i]); break;
+    }
+}
+
+// force vector: 1.0 on [lo, lo+cnt), 0 elsewhere (operators.py:109-113);
+// with sub != nullptr: out = force - sub (schur.py:353)
+__global__ void k_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const double f = (i >= lo && i < lo + cnt) ? 1.0 : 0.0;
+    out[i] = sub ? __dsub_rn(f, sub[i]) : f;
+}
+
+// deterministic two-stage reduction: kind 0 sum(a), 1 dot(a, b)
+__global__ void __launch_bounds__(RED_THREADS) k_reduce1(int kind, const double *a, const double *b,
+                                                         int64_t m, double *part) {
+    __shared__ double sw[RED_THREADS / 32];
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * RED_THREADS)
+        acc = __dadd_rn(acc, kind ? __dmul_rn(a[i], b[i]) : a[i]);
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(~0u, acc, o));
+    if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < RED_THREADS / 32; ++w) s = __dadd_rn(s, sw[w]);
+        part[blockIdx.x] = s;
+    }
+}
+
+__global__ void k_reduce2(const double *part, int nparts, double *out) {
+    double acc = 0.0;
+    for (int j = threadIdx.x; j < nparts; j += 32) acc = __dadd_rn(acc, part[j]);
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(~0u, acc, o));
+    if (threadIdx.x == 0) *out = acc;
+}
+
+// ------------------------------------------------ K8 fused persistent PCG
+
+template <int K>
+__device__ __forceinline__ void grid_sum(double (&v)[K], double *part, cg::grid_group &grid,
+                                         double (*s_warp)[5], double *s_tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double x = v[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(~0u, x, o));
+        if (lane == 0) s_warp[warp][k] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < CG_THREADS / 32; ++w) s = __dadd_rn(s, s_warp[w][threadIdx.x]);
+        part[threadIdx.x * gridDim.x + blockIdx.x] = s;
+    }
+    grid.sync();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = 0.0;
+            for (int j = lane; j < (int)gridDim.x; j += 32) s = __dadd_rn(s, __ldcg(part + k * gridDim.x + j));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(~0u, s, o));
+            if (lane == 0) s_tot[k] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = s_tot[k];
+    __syncthreads();
+}
+
+// OP 0: velocity A with Jacobi diag(A)   (schur.py:200-219)
+// OP 1: S_hat = B diag(A)^-1 B^T with Jacobi diag(S_hat), projected (schur.py:243-272)
+template <int OP, bool PROJ>
+__global__ void __launch_bounds__(CG_THREADS) k_pcg(CgParams P) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double s_tab[40];
+    __shared__ double s_warp[CG_THREADS / 32][5];
+    __shared__ double s_tot[5];
+    if (threadIdx.x < 16) {
+        s_tab[threadIdx.x] = P.diag_code[threadIdx.x];
+        s_tab[16 + threadIdx.x] = P.inv_code[threadIdx.x];
+        if (threadIdx.x < 8) s_tab[32 + threadIdx.x] = P.invA_enc[threadIdx.x];
+    }
+    __syncthreads();
+    const double *sdiag = s_tab, *sinv = s_tab + 16, *sinvA = s_tab + 32;
+    const Geo &g = P.g;
+    const int64_t m = P.m;
+    const int64_t tid = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * CG_THREADS;
+    const double *__restrict__ invS = P.invS;
+    const uint64_t *__restrict__ rec = P.rec;
+    double *x = P.x, *r = P.r;
+
+    auto inv_of = [&](uint64_t rc) -> double {
+        if (OP == 0) return sinv[rec_vcode(rc)];
+        else return invS[rec_pkey(rc)];
+    };
+    auto op_at = [&](uint64_t rc, double vi, auto ld) -> double {
+        if (OP == 0) return apply_A_at(g, rc, vi, sdiag[rec_vcode(rc)], P.inv_h2, ld);
+        else return apply_S_at(g, rc, vi, sinvA, P.inv_h, ld);
+    };
+
+    // ---- setup: project rhs, r = op(x0) - rhs, z = M^-1 r (krylov.py:102-119)
+    double mu_rhs = 0.0, mu = 0.0, rz = 0.0, rp0 = 0.0, ru0 = 0.0;
+    if (PROJ) {
+        double v[1] = {0.0};
+        for (int64_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], P.rhs[i]);
+        grid_sum<1>(v, P.part + 0 * 8 * gridDim.x, grid, s_warp, s_tot);
+        mu_rhs = v[0] / (double)m;
+    }
+    {
+        double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        const double *x0 = P.x0;
+        for (int64_t i = tid; i < m; i += stride) {
+            const uint64_t rc = rec[i];
+            double ax = 0.0, xi = 0.0;
+            if (x0) {
+                xi = x0[i];
+                ax = op_at(rc, xi, [&](uint32_t j) { return x0[j]; });
+            }
+            const double b = PROJ ? __dsub_rn(P.rhs[i], mu_rhs) : P.rhs[i];
+            const double ri = __dsub_rn(ax, b);
+            const double zi = __dmul_rn(ri, inv_of(rc));
+            if (x0 != x) x[i] = xi;
+            r[i] = ri;
+            v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
+            v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
+            v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
+            v[3] = __dadd_rn(v[3], zi);
+            v[4] = __dadd_rn(v[4], ri);
+        }
+        grid_sum<5>(v, P.part + 1 * 8 * gridDim.x, grid, s_warp, s_tot);
+        if (PROJ) {
+            mu = v[3] / (double)m;
+            v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
+            v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
+        }
+        rz = v[0];
+        rp0 = sqrt(v[1]);
+        ru0 = sqrt(v[2]);
+    }
+    const double ref = P.norm_prec ? rp0 : ru0;
+    double beta = 0.0;
+    double rp_last = rp0, ru_last = ru0;
+    int status = 0;
+    double sval = 0.0;
+    int64_t sat = 0, its = 0;
+    bool conv = (ref == 0.0);
+    double *dold = P.d0, *dnew = P.d1;
+    if (!conv) {
+        for (int64_t k = 0; k < P.max_iter; ++k) {
+            if (rz < 0.0) { status = 1; sval = rz; sat = k; break; }
+            if (rz == 0.0) { conv = true; break; }
+            const bool first = (k == 0);
+            // P1: d = z - mu + beta d_old (recomputed at neighbours), q = op(d), d.q
+            double v1[1] = {0.0};
+            for (int64_t i = tid; i < m; i += stride) {
+                auto dval = [&](uint32_t j) -> double {
+                    double zj = __dmul_rn(r[j], inv_of(rec[j]));
+                    if (PROJ) zj = __dsub_rn(zj, mu);
+                    return first ? zj : __dadd_rn(zj, __dmul_rn(beta, dold[j]));
+                };
+                const uint64_t rc = rec[i];
+                double zi = __dmul_rn(r[i], inv_of(rc));
+                if (PROJ) zi = __dsub_rn(zi, mu);
+                const double di = first ? zi : __dadd_rn(zi, __dmul_rn(beta, dold[i]));
+                const double qi = op_at(rc, di, dval);
+                dnew[i] = di;
+                v1[0] = __dadd_rn(v1[0], __dmul_rn(di, qi));
+            }
+            grid_sum<1>(v1, P.part + 2 * 8 * gridDim.x, grid, s_warp, s_tot);
+            const double dq = v1[0];
+            if (dq <= 0.0) { status = 2; sval = dq; sat = k; break; }
+            const double alpha = rz / dq;
+            // P2: q = op(d), x -= alpha d, r -= alpha q, z = M^-1 r, sums
+            double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int64_t i = tid; i < m; i += stride) {
+                const uint64_t rc = rec[i];
+                const double di = dnew[i];
+                const double qi = op_at(rc, di, [&](uint32_t j) { return dnew[j]; });
+                const double xi = __dsub_rn(x[i], __dmul_rn(alpha, di));
+                const double ri = __dsub_rn(r[i], __dmul_rn(alpha, qi));
+                const double zi = __dmul_rn(ri, inv_of(rc));
+                x[i] = xi;
+                r[i] = ri;
+                v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
+                v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
+                v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
+                v[3] = __dadd_rn(v[3], zi);
+                v[4] = __dadd_rn(v[4], ri);
+            }
+            grid_sum<5>(v, P.part + 3 * 8 * gridDim.x, grid, s_warp, s_tot);
+            if (PROJ) {
+                mu = v[3] / (double)m;
+                v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
+                v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
+            }
+            const double rz_new = v[0];
+            beta = rz_new / rz;
+            rz = rz_new;
+            const double nz = sqrt(v[1]), nr = sqrt(v[2]);
+            if (!(isfinite(nz) && isfinite(nr))) { status = 3; sat = k + 1; break; }
+            its = k + 1;
+            rp_last = nz;
+            ru_last = nr;
+            double *t = dold; dold = dnew; dnew = t;
+            if ((P.norm_prec ? nz : nr) / ref < P.tol) { conv = true; break; }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        CgOut *o = P.out;
+        o->iterations = its;
+        o->converged = conv ? 1 : 0;
+        o->status = status;
+        o->value = sval;
+        o->at_iter = sat;
+        o->res_prec0 = rp0;
+        o->res_unprec0 = ru0;
+        o->res_prec_last = rp_last;
+        o->res_unprec_last = ru_last;
+    }
+}
+
+// ------------------------------------------------------------ launchers
+
+static inline unsigned nblk(int64_t m, int t = 256) { return (unsigned)((m + t - 1) / t); }
+
+void launch_pack_fluid(const uint8_t *fluid, const Geo &g, int64_t nwords, uint32_t *fbits, cudaStream_t s) {
+    k_pack_fluid<<<nblk(nwords), 256, 0, s>>>(fluid, g, nwords, fbits);
+}
+void launch_face_bits(const Geo &g, int a, int64_t nwords, uint32_t *out, cudaStream_t s) {
+    k_face_bits<<<nblk(nwords), 256, 0, s>>>(g, a, nwords, out);
+}
+cudaError_t build_meta(const uint32_t *bits, int64_t nwords, uint32_t off, uint2 *meta, uint32_t *scratch_cnt,
+                       uint32_t *scratch_base, void *temp, size_t temp_bytes, cudaStream_t s) {
+    k_popc<<<nblk(nwords), 256, 0, s>>>(bits, nwords, scratch_cnt);
+    size_t tb = temp_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, tb, scratch_cnt, scratch_base, (int64_t)nwords, s);
+    if (e != cudaSuccess) return e;
+    k_make_meta<<<nblk(nwords), 256, 0, s>>>(bits, scratch_base, off, nwords, meta);
+    return cudaGetLastError();
+}
+size_t scan_temp_bytes(int64_t nwords) {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)nwords);
+    return tb;
+}
+void launch_vel_records(const Geo &g, int a, int64_t nwords, uint64_t *rec, cudaStream_t s) {
+    k_vel_records<<<nblk(nwords), 256, 0, s>>>(g, a, nwords, rec);
+}
+void launch_p_records(const Geo &g, int64_t nwords, uint64_t *rec, cudaStream_t s) {
+    k_p_records<<<nblk(nwords), 256, 0, s>>>(g, nwords, rec);
+}
+void launch_bits_to_u8(const uint2 *meta, const uint32_t *bits, const Geo &g, int64_t ncells, uint8_t *out,
+                       cudaStream_t s) {
+    k_bits_to_u8<<<nblk(ncells), 256, 0, s>>>(meta, bits, g, ncells, out);
+}
+void launch_vcodes(const uint64_t *rec, int64_t m, uint8_t *out, cudaStream_t s) {
+    if (m) k_vcodes<<<nblk(m), 256, 0, s>>>(rec, m, out);
+}
+void launch_zero_sdiag(const uint64_t *prec, int64_t m, int *flag, cudaStream_t s) {
+    if (m) k_zero_sdiag<<<nblk(m), 256, 0, s>>>(prec, m, flag);
+}
+void launch_apply_A(const Geo &g, const uint64_t *rec, const double *u, double *out, int64_t m,
+                    const double *diag_code, double inv_h2, cudaStream_t s) {
+    if (m) k_apply_A<<<nblk(m), 256, 0, s>>>(g, rec, u, out, m, diag_code, inv_h2);
+}
+void launch_apply_div(const Geo &g, const uint64_t *prec, const double *u, double *out, int64_t m, double inv_h,
+                      cudaStream_t s) {
+    if (m) k_apply_div<<<nblk(m), 256, 0, s>>>(g, prec, u, out, m, inv_h);
+}
+void launch_apply_grad(const Geo &g, const uint64_t *vrec, const double *p, double *out, int64_t m,
+                       double inv_h, cudaStream_t s) {
+    if (m) k_apply_grad<<<nblk(m), 256, 0, s>>>(g, vrec, p, out, m, inv_h);
+}
+void launch_apply_S(const Geo &g, const uint64_t *prec, const double *p, double *out, int64_t m,
+                    const double *invA_enc, double inv_h, cudaStream_t s) {
+    if (m) k_apply_S<<<nblk(m), 256, 0, s>>>(g, prec, p, out, m, invA_enc, inv_h);
+}
+void launch_dwd(const Geo &g, const uint64_t *prec, const double *w, double *out, int64_t m, double inv_h2,
+                cudaStream_t s) {
+    if (m) k_dwd<<<nblk(m), 256, 0, s>>>(g, prec, w, out, m, inv_h2);
+}
+void launch_vec(int kind, double *out, double *a, const double *b, double sc, int64_t m, cudaStream_t s) {
+    if (m) k_vec<<<nblk(m), 256, 0, s>>>(kind, out, a, b, sc, m);
+}
+void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s) {
+    if (m) k_force<<<nblk(m), 256, 0, s>>>(out, sub, lo, cnt, m);
+}
+int launch_reduce(int kind, const double *a, const double *b, int64_t m, double *part, double *out,
+                  cudaStream_t s) {
+    int nb = (int)std::min<int64_t>(RED_MAX_BLOCKS, std::max<int64_t>(1, (m + 4 * RED_THREADS - 1) / (4 * RED_THREADS)));
+    k_reduce1<<<nb, RED_THREADS, 0, s>>>(kind, a, b, m, part);
+    k_reduce2<<<1, 32, 0, s>>>(part, nb, out);
+    return 2;
+}
+
+template <int OP, bool PROJ>
+static const void *pcg_fn() { return (const void *)k_pcg<OP, PROJ>; }
+
+int pcg_max_grid(int op, int proj, int device) {
+    const void *fn = op == 0 ? pcg_fn<0, false>() : (proj ? pcg_fn<1, true>() : pcg_fn<1, false>());
+    int per_sm = 0, nsm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CG_THREADS, 0);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    return per_sm * nsm;
+}
+
+cudaError_t launch_pcg(int op, int proj, CgParams &P, int grid, cudaStream_t s) {
+    const void *fn = op == 0 ? pcg_fn<0, false>() : (proj ? pcg_fn<1, true>() : pcg_fn<1, false>());
+    void *args[] = {&P};
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(CG_THREADS), args, 0, s);
+}
+
+}  // namespace vs
