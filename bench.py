@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the Schur-complement Stokes path (BASELINE.json metric).
+
+Workload (N=1): BASELINE configs[1] -- 64^3 periodic sphere packing
+(radii U[4,8], porosity 0.4, x-percolating component), f=(1,0,0), solved
+once with Uzawa and once with SIMPLE at eps_S=1e-8, eps_A=eps_Shat=1e-12
+(SURVEY Appendix B).  One "step" = those two full Schur solves to tolerance.
+
+* value     -- masked-stencil Gcell/s = n^3 * (I_A + I_S) / t_device, I_A
+               counting every inner A-iteration (incl. the u_f solve),
+               I_S every inner S_hat-iteration; t_device = CUDA-event time
+               of the solves with the geometry resident in HBM.
+* e2e       -- same metric through the public API with host buffers:
+               assemble(host mask) (H2D + device geometry build) and
+               solve_schur returning p, u (D2H) inside the timed region.
+* roofline  -- dominant kernel (fused persistent PCG): algorithmic bytes
+               64 B per DOF per CG iteration x DOF-iterations
+               / summed CUDA-event launch time, vs MEASURED_PEAKS hbm_gbs.
+* cpu_baseline / --impl reference -- the CPU oracle port (oracle/, the
+               reference algorithm restated in numpy) on the host cores.
+
+Multi-GPU (torchrun): replicas only for now -- each rank solves its own
+copy (no data-path collective); value sums the ranks' work over the max
+device time ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+TOL = dict(eps_S=1e-8, eps_A=1e-12, eps_Shat=1e-12)
+BYTES_PER_DOF_ITER = 64  # x, r, d read+write, r and d re-read
+METRIC = "masked-stencil Gcell/s & HBM GB/s (vs 8 TB/s); Schur solve time-to-tol at 1-8 GPU"
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.dev)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------- CPU oracle leg
+def _oracle_sample(args):
+    """One bounded sample of the workload on the CPU oracle: a SIMPLE
+    solve_schur capped at one outer iteration (u_f solve, initial S_hat
+    solve, one outer step = A-solve + S_hat-solve, refresh)."""
+    key, seed = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    sys.path.insert(0, ROOT)
+    from oracle import voxoracle as vo
+    from paper_2307_05266_b200 import configs
+
+    grid = configs.make_geometry(key, seed)
+    s = vo.build_system(grid.fluid, 0)
+    t0 = time.perf_counter()
+    rep = vo.solve_schur(s, "simple", max_iter=1, **TOL)
+    dt = time.perf_counter() - t0
+    ia = rep["inner_iter_totals"]["velocity"] + rep["uf_iters"]
+    isx = rep["inner_iter_totals"]["preconditioner"]
+    # the initial preconditioner solve is inside solve_schur too
+    return dict(cells_iters=grid.fluid.size * (ia + isx), seconds=dt, I_A=ia, I_S=isx)
+
+
+def cpu_sample(key, seed, procs):
+    if procs <= 1:
+        res = [_oracle_sample((key, seed))]
+    else:
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(procs) as pool:
+            res = pool.map(_oracle_sample, [(key, seed)] * procs)
+    tmax = max(r["seconds"] for r in res)
+    tot = sum(r["cells_iters"] for r in res)
+    return tot / tmax / 1e9, res
+
+
+def usable_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(a):
+    rank, _, world = env_rank()
+    if rank != 0:
+        return 0
+    cores = usable_cores()
+    vals = []
+    for i in range(a.warmup + a.steps):
+        v, res = cpu_sample(a.config, a.seed, cores)
+        if i >= a.warmup:
+            vals.append(v)
+    val = statistics.median(vals)
+    spec = __import__("paper_2307_05266_b200.configs", fromlist=["CONFIGS"]).CONFIGS[a.config]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "Gcell/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": spec.name, "seed": a.seed, "precs": list(spec.precs)},
+        "cpu_baseline": {"value": val, "unit": "Gcell/s", "cores": cores, "kind": "port",
+                         "sample": "per process: oracle SIMPLE solve_schur capped at 1 outer "
+                                   "iteration on the same geometry; one process per core"},
+        "e2e": {"value": val, "unit": "Gcell/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(a):
+    rank, local, world = env_rank()
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        torch.cuda.set_device(local)
+        dist_mod.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist = dist_mod
+    dev = local
+    torch.cuda.set_device(dev)
+    import paper_2307_05266_b200 as vx
+    from paper_2307_05266_b200 import configs
+
+    spec = configs.CONFIGS[a.config]
+    grid = configs.make_geometry(a.config, a.seed)
+    ncell = grid.fluid.size
+    cfgs = [vx.SchurConfig(prec=p, max_iter=spec.max_iter, **TOL) for p in spec.precs]
+    sys_ = vx.assemble(grid, 0, check_connectivity=spec.check_connectivity, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{dev}")  # 256 MB > L2
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+
+    def one_step(s):
+        agg = dict(ms=0.0, IA=0, IS=0, dofA=0, dofS=0, msA=0.0, msS=0.0, launches=0,
+                   lA=0, lS=0, reps=[])
+        for cfg in cfgs:
+            rep = vx.solve_schur(s, cfg, return_fields=False)
+            st = vx.last_kernel_stats(s)
+            agg["ms"] += rep.device_ms
+            rtot = rep.inner_iter_totals
+            agg["IA"] += st["velocity_cg"]["iterations"]
+            agg["IS"] += st["simple_cg"]["iterations"]
+            agg["dofA"] += st["velocity_cg"]["dof_iters"]
+            agg["dofS"] += st["simple_cg"]["dof_iters"]
+            agg["msA"] += st["velocity_cg"]["ms"]
+            agg["msS"] += st["simple_cg"]["ms"]
+            agg["lA"] += st["velocity_cg"]["launches"]
+            agg["lS"] += st["simple_cg"]["launches"]
+            agg["launches"] += st["kernel_launches"]
+            agg["reps"].append(dict(prec=cfg.prec, iters_outer=rep.iters_outer,
+                                    inner=rtot, k=rep.k_value, converged=rep.converged,
+                                    device_ms=rep.device_ms))
+        return agg
+
+    for _ in range(a.warmup):
+        one_step(sys_)
+    barrier()
+    steps = []
+    with ClockSampler(dev) as clk:
+        for _ in range(a.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            steps.append(one_step(sys_))
+        barrier()
+    tot = {k: sum(st[k] for st in steps) for k in
+           ("ms", "IA", "IS", "dofA", "dofS", "msA", "msS", "launches", "lA", "lS")}
+    t_dev = tot["ms"] / 1e3
+    cells_iters = ncell * (tot["IA"] + tot["IS"])
+    # whole-job aggregate over ranks, max device time over ranks
+    if dist is not None:
+        tt = torch.tensor([t_dev, cells_iters], dtype=torch.float64, device=f"cuda:{dev}")
+        tmax = tt[0:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:2], op=dist.ReduceOp.SUM)
+        t_job, cells_job = float(tmax.item()), float(tt[1].item())
+    else:
+        t_job, cells_job = t_dev, cells_iters
+    value = cells_job / t_job / 1e9
+    alg_bytes = BYTES_PER_DOF_ITER * (tot["dofA"] + tot["dofS"])
+    hbm_alg = alg_bytes / t_dev / 1e9
+
+    # e2e through the public API with host buffers (H2D mask, D2H p, u)
+    e2e_t, e2e_cells, h2d, d2h = 0.0, 0, 0, 0
+    for _ in range(max(1, a.steps)):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        s2 = vx.assemble(grid, 0, check_connectivity=spec.check_connectivity, device=dev)
+        for cfg in cfgs:
+            rep = vx.solve_schur(s2, cfg, return_fields=True)
+            st = vx.last_kernel_stats(s2)
+            e2e_cells += ncell * (st["velocity_cg"]["iterations"] + st["simple_cg"]["iterations"])
+            d2h += rep.pressure.nbytes + rep.velocity.nbytes + 5 * 8 * (rep.iters_outer + 1)
+        e2e_t += time.perf_counter() - t0
+        h2d += grid.fluid.size  # uint8 mask
+        del s2
+    nsteps_e2e = max(1, a.steps)
+    e2e = {"value": e2e_cells / e2e_t / 1e9, "unit": "Gcell/s",
+           "h2d_bytes_per_step": h2d // nsteps_e2e, "d2h_bytes_per_step": d2h // nsteps_e2e,
+           "ms_per_step": 1e3 * e2e_t / nsteps_e2e,
+           "includes": "assemble (host connectivity check + H2D mask + device geometry build) "
+                       "+ solves + D2H p,u,histories"}
+
+    # dominant kernel: the fused persistent PCG with the larger share
+    domS = tot["msS"] >= tot["msA"]
+    dof_k, ms_k, l_k = (tot["dofS"], tot["msS"], tot["lS"]) if domS else (tot["dofA"], tot["msA"], tot["lA"])
+    peak, peak_kind = measured_peak()
+    achieved = BYTES_PER_DOF_ITER * dof_k / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        traffic = tj.get(a.config, {}).get("k_pcg_S" if domS else "k_pcg_A")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k_pcg<S_hat,proj> (fused persistent PCG)" if domS else "k_pcg<A> (fused persistent PCG)",
+                "launches": l_k, "avg_launch_ms": ms_k / max(1, l_k),
+                "bytes_per_launch": BYTES_PER_DOF_ITER * dof_k / max(1, l_k),
+                "peak_kind": peak_kind, "frac_vs_8TBs": achieved / 8000.0,
+                "share_of_step": (ms_k / tot["ms"]) if tot["ms"] else None}
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not a.no_cpu:
+            cv, res = cpu_sample(a.config, a.seed, 1)
+            cpu = {"value": cv, "unit": "Gcell/s", "cores": 1, "kind": "port",
+                   "sample": f"oracle (numpy port of the reference) SIMPLE solve_schur capped at 1 outer "
+                             f"iteration on the same geometry: {res[0]['I_A']} A-its + {res[0]['I_S']} "
+                             f"S_hat-its in {res[0]['seconds']:.1f} s, 1 core"}
+        last = steps[-1]["reps"]
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gcell/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * t_job / a.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": spec.name, "seed": a.seed, "n": grid.n,
+                       "porosity": float(grid.fluid.mean()), "m_u": sys_.m_u, "m_p": sys_.m_p,
+                       "precs": list(spec.precs), "tolerances": TOL,
+                       "step": "one full solve_schur to tolerance per preconditioner",
+                       "l2": "256 MB buffer written between timed steps (L2 flushed)",
+                       "parallelism": f"replicas{world}" if world > 1 else "single"},
+            "hbm_gbs_algorithmic": hbm_alg,
+            "time_to_tol_ms": {r["prec"]: r["device_ms"] for r in last},
+            "solves": last,
+            "inner_iterations_per_step": {"A": tot["IA"] // a.steps, "S_hat": tot["IS"] // a.steps},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": tot["launches"], "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        print("warning: the timing rules require --warmup >= 3", file=sys.stderr)
+    sys.exit(run_reference(a) if a.impl == "reference" else run_ours(a))
+
+
+if __name__ == "__main__":
+    main()

@@ -70,6 +70,15 @@ const char *vs_version(void);
 int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels,
                   int64_t *n_components);
 
+/* Seeded synthetic geometry (BASELINE configs; not a reference function):
+ * solidify, in order, the periodic balls (or, with prism_axis >= 0,
+ * cylinders along that axis) of the given centres/radii (cell-index
+ * coordinates, minimum-image distance <= r) until the fluid count drops
+ * to target_fluid or the list ends.  *used = balls consumed. */
+int vs_stamp_balls(uint8_t *fluid, int dim, int n, const double *centers,
+                   const double *radii, int64_t count, int64_t target_fluid,
+                   int prism_axis, int64_t *used, int64_t *n_fluid);
+
 /* assemble() (operators.py:209-302): validation, connectivity check, and
  * the on-device geometry build (face masks, DOF ranks, diag codes).
  * inv_h = 1.0/h and inv_h2 = 1.0/h**2 as the reference computes them

@@ -72,6 +72,8 @@ def _load():
         "vs_last_error": (C.c_char_p, []),
         "vs_version": (C.c_char_p, []),
         "vs_components": (C.c_int, [u8, C.c_int, C.c_int, P, i64p]),
+        "vs_stamp_balls": (C.c_int, [P, C.c_int, C.c_int, P, P, C.c_int64, C.c_int64, C.c_int,
+                                     i64p, i64p]),
         "vs_ctx_create": (C.c_int, [u8, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.c_double, C.c_double, C.POINTER(P)]),
         "vs_ctx_destroy": (None, [P]),
@@ -97,7 +99,7 @@ def _load():
 
 lib = _load()
 EXPORTED = (
-    "vs_last_error", "vs_version", "vs_components", "vs_ctx_create", "vs_ctx_destroy",
+    "vs_last_error", "vs_version", "vs_components", "vs_stamp_balls", "vs_ctx_create", "vs_ctx_destroy",
     "vs_counts", "vs_export_geometry", "vs_apply_laplacian", "vs_apply_divergence",
     "vs_apply_gradient", "vs_divergence_weighted_diagonal", "vs_apply_simple",
     "vs_solve_velocity", "vs_solve_simple", "vs_solve_schur", "vs_kernel_stats",

@@ -303,6 +303,48 @@ int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels, int64_t
     return VS_OK;
 }
 
+int vs_stamp_balls(uint8_t *fluid, int dim, int n, const double *centers, const double *radii, int64_t count,
+                   int64_t target_fluid, int prism_axis, int64_t *used, int64_t *n_fluid) {
+    if ((dim != 2 && dim != 3) || n < 2) return fail(VS_EVALUE, "bad grid for vs_stamp_balls");
+    const int64_t N = dim == 3 ? (int64_t)n * n * n : (int64_t)n * n;
+    int64_t nf = 0;
+    for (int64_t i = 0; i < N; ++i) nf += fluid[i] ? 1 : 0;
+    int64_t k = 0;
+    const int64_t st[3] = {dim == 3 ? (int64_t)n * n : (int64_t)n, dim == 3 ? (int64_t)n : 1, 1};
+    for (; k < count && nf > target_fluid; ++k) {
+        const double r = radii[k], r2 = r * r;
+        const double *c = centers + k * dim;
+        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+        for (int a = 0; a < dim; ++a) {
+            if (a == prism_axis) { lo[a] = 0; hi[a] = n - 1; continue; }
+            lo[a] = (int)std::floor(c[a] - r) - 1;
+            hi[a] = (int)std::ceil(c[a] + r) + 1;
+            if (hi[a] - lo[a] + 1 > n) { lo[a] = 0; hi[a] = n - 1; }
+        }
+        if (dim == 2) { lo[2] = hi[2] = 0; }
+        for (int i = lo[0]; i <= hi[0]; ++i)
+            for (int j = lo[1]; j <= hi[1]; ++j)
+                for (int l = lo[2]; l <= hi[2]; ++l) {
+                    const int idx[3] = {i, j, l};
+                    double d2 = 0.0;
+                    int64_t off = 0;
+                    for (int a = 0; a < dim; ++a) {
+                        const int w = ((idx[a] % n) + n) % n;  // periodic wrap of the window
+                        off += w * st[dim == 3 ? a : (a == 0 ? 0 : 2)];
+                        if (a == prism_axis) continue;
+                        double dd = std::fabs((double)w - c[a]);
+                        dd = std::min(dd, (double)n - dd);  // minimum image
+                        d2 += dd * dd;
+                    }
+                    if (d2 <= r2 && fluid[off]) { fluid[off] = 0; --nf; }
+                }
+        if (nf <= target_fluid) { ++k; break; }
+    }
+    *used = k;
+    *n_fluid = nf;
+    return VS_OK;
+}
+
 int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_connectivity, int require_walls,
                   int device, double inv_h, double inv_h2, vs_ctx **out) {
     *out = nullptr;
