@@ -71,9 +71,10 @@ struct vs_ctx {
     uint64_t *vrec = nullptr, *prec = nullptr;
     double *invS = nullptr, *d_diag_code = nullptr, *d_invA_enc = nullptr;
     // velocity work vectors
-    double *u_rhs, *u_w, *u_iter, *u_f, *u_r, *u_d0, *u_d1, *u_tmp;
+    double *u_rhs, *u_w, *u_iter, *u_f, *u_r, *u_z, *u_d0, *u_d1, *u_tmp;
     // pressure work vectors
-    double *p_x, *p_r, *p_d, *p_z, *p_q, *p_b, *p_sr, *p_sd0, *p_sd1, *p_tmp;
+    double *p_x, *p_r, *p_d, *p_z, *p_q, *p_b, *p_sr, *p_sz, *p_sd0, *p_sd1, *p_tmp;
+    unsigned *bar = nullptr;
     double *part = nullptr, *red_part = nullptr, *scal = nullptr;
     CgOut *cgout = nullptr;
     double *h_scal = nullptr;  // pinned
@@ -220,6 +221,8 @@ int64_t cg_solve(vs_ctx *c, int op, const double *rhs, const double *x0, double 
     P.x0 = x0;
     P.x = x;
     P.r = op == 0 ? c->u_r : c->p_sr;
+    P.z = op == 0 ? c->u_z : c->p_sz;
+    P.bar = c->bar;
     P.d0 = op == 0 ? c->u_d0 : c->p_sd0;
     P.d1 = op == 0 ? c->u_d1 : c->p_sd1;
     P.part = c->part;
@@ -236,7 +239,7 @@ int64_t cg_solve(vs_ctx *c, int op, const double *rhs, const double *x0, double 
     const int gmax = op == 0 ? c->grid_A : c->grid_S;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (m + CG_THREADS - 1) / CG_THREADS));
     CK(cudaEventRecord(c->evs0, c->stream));
-    CK(launch_pcg(op, op == 1 ? 1 : 0, P, grid, c->stream));
+    CK(launch_pcg(c->dim, op, P, grid, c->stream));
     CK(cudaEventRecord(c->evs1, c->stream));
     ++c->launches;
     CK(cudaMemcpyAsync(c->h_cg, c->cgout, sizeof(CgOut), cudaMemcpyDeviceToHost, c->stream));
@@ -474,13 +477,15 @@ int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_
         C->sdiag_ok = hflag == 0;
         // ---- work vectors
         const int64_t mu = C->m_u, mp = C->m_p;
-        for (double **v : {&C->u_rhs, &C->u_w, &C->u_iter, &C->u_f, &C->u_r, &C->u_d0, &C->u_d1, &C->u_tmp})
+        for (double **v : {&C->u_rhs, &C->u_w, &C->u_iter, &C->u_f, &C->u_r, &C->u_z, &C->u_d0, &C->u_d1, &C->u_tmp})
             *v = C->alloc<double>(mu);
-        for (double **v : {&C->p_x, &C->p_r, &C->p_d, &C->p_z, &C->p_q, &C->p_b, &C->p_sr, &C->p_sd0, &C->p_sd1,
-                           &C->p_tmp})
+        for (double **v : {&C->p_x, &C->p_r, &C->p_d, &C->p_z, &C->p_q, &C->p_b, &C->p_sr, &C->p_sz, &C->p_sd0,
+                           &C->p_sd1, &C->p_tmp})
             *v = C->alloc<double>(mp);
-        C->grid_A = pcg_max_grid(0, 0, device);
-        C->grid_S = pcg_max_grid(1, 1, device);
+        C->grid_A = pcg_max_grid(dim, 0, device);
+        C->grid_S = pcg_max_grid(dim, 1, device);
+        C->bar = C->alloc<unsigned>(2);
+        CK(cudaMemsetAsync(C->bar, 0, 2 * sizeof(unsigned), C->stream));
         C->part = C->alloc<double>((size_t)4 * 8 * std::max(C->grid_A, C->grid_S));
         C->red_part = C->alloc<double>(RED_MAX_BLOCKS);
         C->scal = C->alloc<double>(8);

@@ -7,7 +7,7 @@
 
 namespace vs {
 
-constexpr int CG_THREADS = 256;
+constexpr int CG_THREADS = 512;
 constexpr int RED_THREADS = 256;
 constexpr int RED_MAX_BLOCKS = 592;
 
@@ -25,8 +25,9 @@ struct CgParams {
     int64_t m;
     const uint64_t *rec;
     const double *rhs, *x0;
-    double *x, *r, *d0, *d1;
+    double *x, *r, *z, *d0, *d1;
     double *part;  // 4 sets x 8 slots x grid
+    unsigned *bar; // grid barrier {count, generation}
     CgOut *out;
     double tol;
     int64_t max_iter;
@@ -63,7 +64,7 @@ void launch_vec(int kind, double *out, double *a, const double *b, double sc, in
 void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s);
 int launch_reduce(int kind, const double *a, const double *b, int64_t m, double *part, double *out,
                   cudaStream_t s);
-int pcg_max_grid(int op, int proj, int device);
-cudaError_t launch_pcg(int op, int proj, CgParams &P, int grid, cudaStream_t s);
+int pcg_max_grid(int dim, int op, int device);
+cudaError_t launch_pcg(int dim, int op, CgParams &P, int grid, cudaStream_t s);
 
 }  // namespace vs

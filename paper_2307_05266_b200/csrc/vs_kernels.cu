@@ -2,16 +2,12 @@
 //
 //   K1  geometry build   (operators.py:232-297)  integer, bit-exact
 //   K2-K6 operator applies (operators.py:131-206, schur.py:234-240) bit-exact
-//   K8  fused persistent PCG (krylov.py:76-182) for A and S_hat: two passes
-//       per iteration, device-resident scalars, deterministic grid reductions
+//   (K8, the fused persistent PCG, lives in vs_cg.cu)
 //   outer-loop vector kernels + deterministic reductions (schur.py:291-385)
-#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "vs_device.cuh"
 #include "vs_internal.h"
-
-namespace cg = cooperative_groups;
 
 namespace vs {
 
@@ -257,196 +253,6 @@ __global__ void k_reduce2(const double *part, int nparts, double *out) {
     if (threadIdx.x == 0) *out = acc;
 }
 
-// ------------------------------------------------ K8 fused persistent PCG
-
-template <int K>
-__device__ __forceinline__ void grid_sum(double (&v)[K], double *part, cg::grid_group &grid,
-                                         double (*s_warp)[5], double *s_tot) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        double x = v[k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(~0u, x, o));
-        if (lane == 0) s_warp[warp][k] = x;
-    }
-    __syncthreads();
-    if (threadIdx.x < K) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < CG_THREADS / 32; ++w) s = __dadd_rn(s, s_warp[w][threadIdx.x]);
-        part[threadIdx.x * gridDim.x + blockIdx.x] = s;
-    }
-    grid.sync();
-    if (warp == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double s = 0.0;
-            for (int j = lane; j < (int)gridDim.x; j += 32) s = __dadd_rn(s, __ldcg(part + k * gridDim.x + j));
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(~0u, s, o));
-            if (lane == 0) s_tot[k] = s;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = s_tot[k];
-    __syncthreads();
-}
-
-// OP 0: velocity A with Jacobi diag(A)   (schur.py:200-219)
-// OP 1: S_hat = B diag(A)^-1 B^T with Jacobi diag(S_hat), projected (schur.py:243-272)
-template <int OP, bool PROJ>
-__global__ void __launch_bounds__(CG_THREADS) k_pcg(CgParams P) {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double s_tab[40];
-    __shared__ double s_warp[CG_THREADS / 32][5];
-    __shared__ double s_tot[5];
-    if (threadIdx.x < 16) {
-        s_tab[threadIdx.x] = P.diag_code[threadIdx.x];
-        s_tab[16 + threadIdx.x] = P.inv_code[threadIdx.x];
-        if (threadIdx.x < 8) s_tab[32 + threadIdx.x] = P.invA_enc[threadIdx.x];
-    }
-    __syncthreads();
-    const double *sdiag = s_tab, *sinv = s_tab + 16, *sinvA = s_tab + 32;
-    const Geo &g = P.g;
-    const int64_t m = P.m;
-    const int64_t tid = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x;
-    const int64_t stride = (int64_t)gridDim.x * CG_THREADS;
-    const double *__restrict__ invS = P.invS;
-    const uint64_t *__restrict__ rec = P.rec;
-    double *x = P.x, *r = P.r;
-
-    auto inv_of = [&](uint64_t rc) -> double {
-        if (OP == 0) return sinv[rec_vcode(rc)];
-        else return invS[rec_pkey(rc)];
-    };
-    auto op_at = [&](uint64_t rc, double vi, auto ld) -> double {
-        if (OP == 0) return apply_A_at(g, rc, vi, sdiag[rec_vcode(rc)], P.inv_h2, ld);
-        else return apply_S_at(g, rc, vi, sinvA, P.inv_h, ld);
-    };
-
-    // ---- setup: project rhs, r = op(x0) - rhs, z = M^-1 r (krylov.py:102-119)
-    double mu_rhs = 0.0, mu = 0.0, rz = 0.0, rp0 = 0.0, ru0 = 0.0;
-    if (PROJ) {
-        double v[1] = {0.0};
-        for (int64_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], P.rhs[i]);
-        grid_sum<1>(v, P.part + 0 * 8 * gridDim.x, grid, s_warp, s_tot);
-        mu_rhs = v[0] / (double)m;
-    }
-    {
-        double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        const double *x0 = P.x0;
-        for (int64_t i = tid; i < m; i += stride) {
-            const uint64_t rc = rec[i];
-            double ax = 0.0, xi = 0.0;
-            if (x0) {
-                xi = x0[i];
-                ax = op_at(rc, xi, [&](uint32_t j) { return x0[j]; });
-            }
-            const double b = PROJ ? __dsub_rn(P.rhs[i], mu_rhs) : P.rhs[i];
-            const double ri = __dsub_rn(ax, b);
-            const double zi = __dmul_rn(ri, inv_of(rc));
-            if (x0 != x) x[i] = xi;
-            r[i] = ri;
-            v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
-            v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
-            v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
-            v[3] = __dadd_rn(v[3], zi);
-            v[4] = __dadd_rn(v[4], ri);
-        }
-        grid_sum<5>(v, P.part + 1 * 8 * gridDim.x, grid, s_warp, s_tot);
-        if (PROJ) {
-            mu = v[3] / (double)m;
-            v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
-            v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
-        }
-        rz = v[0];
-        rp0 = sqrt(v[1]);
-        ru0 = sqrt(v[2]);
-    }
-    const double ref = P.norm_prec ? rp0 : ru0;
-    double beta = 0.0;
-    double rp_last = rp0, ru_last = ru0;
-    int status = 0;
-    double sval = 0.0;
-    int64_t sat = 0, its = 0;
-    bool conv = (ref == 0.0);
-    double *dold = P.d0, *dnew = P.d1;
-    if (!conv) {
-        for (int64_t k = 0; k < P.max_iter; ++k) {
-            if (rz < 0.0) { status = 1; sval = rz; sat = k; break; }
-            if (rz == 0.0) { conv = true; break; }
-            const bool first = (k == 0);
-            // P1: d = z - mu + beta d_old (recomputed at neighbours), q = op(d), d.q
-            double v1[1] = {0.0};
-            for (int64_t i = tid; i < m; i += stride) {
-                auto dval = [&](uint32_t j) -> double {
-                    double zj = __dmul_rn(r[j], inv_of(rec[j]));
-                    if (PROJ) zj = __dsub_rn(zj, mu);
-                    return first ? zj : __dadd_rn(zj, __dmul_rn(beta, dold[j]));
-                };
-                const uint64_t rc = rec[i];
-                double zi = __dmul_rn(r[i], inv_of(rc));
-                if (PROJ) zi = __dsub_rn(zi, mu);
-                const double di = first ? zi : __dadd_rn(zi, __dmul_rn(beta, dold[i]));
-                const double qi = op_at(rc, di, dval);
-                dnew[i] = di;
-                v1[0] = __dadd_rn(v1[0], __dmul_rn(di, qi));
-            }
-            grid_sum<1>(v1, P.part + 2 * 8 * gridDim.x, grid, s_warp, s_tot);
-            const double dq = v1[0];
-            if (dq <= 0.0) { status = 2; sval = dq; sat = k; break; }
-            const double alpha = rz / dq;
-            // P2: q = op(d), x -= alpha d, r -= alpha q, z = M^-1 r, sums
-            double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            for (int64_t i = tid; i < m; i += stride) {
-                const uint64_t rc = rec[i];
-                const double di = dnew[i];
-                const double qi = op_at(rc, di, [&](uint32_t j) { return dnew[j]; });
-                const double xi = __dsub_rn(x[i], __dmul_rn(alpha, di));
-                const double ri = __dsub_rn(r[i], __dmul_rn(alpha, qi));
-                const double zi = __dmul_rn(ri, inv_of(rc));
-                x[i] = xi;
-                r[i] = ri;
-                v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
-                v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
-                v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
-                v[3] = __dadd_rn(v[3], zi);
-                v[4] = __dadd_rn(v[4], ri);
-            }
-            grid_sum<5>(v, P.part + 3 * 8 * gridDim.x, grid, s_warp, s_tot);
-            if (PROJ) {
-                mu = v[3] / (double)m;
-                v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
-                v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
-            }
-            const double rz_new = v[0];
-            beta = rz_new / rz;
-            rz = rz_new;
-            const double nz = sqrt(v[1]), nr = sqrt(v[2]);
-            if (!(isfinite(nz) && isfinite(nr))) { status = 3; sat = k + 1; break; }
-            its = k + 1;
-            rp_last = nz;
-            ru_last = nr;
-            double *t = dold; dold = dnew; dnew = t;
-            if ((P.norm_prec ? nz : nr) / ref < P.tol) { conv = true; break; }
-        }
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        CgOut *o = P.out;
-        o->iterations = its;
-        o->converged = conv ? 1 : 0;
-        o->status = status;
-        o->value = sval;
-        o->at_iter = sat;
-        o->res_prec0 = rp0;
-        o->res_unprec0 = ru0;
-        o->res_prec_last = rp_last;
-        o->res_unprec_last = ru_last;
-    }
-}
-
 // ------------------------------------------------------------ launchers
 
 static inline unsigned nblk(int64_t m, int t = 256) { return (unsigned)((m + t - 1) / t); }
@@ -519,23 +325,6 @@ int launch_reduce(int kind, const double *a, const double *b, int64_t m, double 
     k_reduce1<<<nb, RED_THREADS, 0, s>>>(kind, a, b, m, part);
     k_reduce2<<<1, 32, 0, s>>>(part, nb, out);
     return 2;
-}
-
-template <int OP, bool PROJ>
-static const void *pcg_fn() { return (const void *)k_pcg<OP, PROJ>; }
-
-int pcg_max_grid(int op, int proj, int device) {
-    const void *fn = op == 0 ? pcg_fn<0, false>() : (proj ? pcg_fn<1, true>() : pcg_fn<1, false>());
-    int per_sm = 0, nsm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CG_THREADS, 0);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    return per_sm * nsm;
-}
-
-cudaError_t launch_pcg(int op, int proj, CgParams &P, int grid, cudaStream_t s) {
-    const void *fn = op == 0 ? pcg_fn<0, false>() : (proj ? pcg_fn<1, true>() : pcg_fn<1, false>());
-    void *args[] = {&P};
-    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(CG_THREADS), args, 0, s);
 }
 
 }  // namespace vs
