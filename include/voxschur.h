@@ -134,6 +134,11 @@ typedef struct {
 int vs_kernel_stats(vs_ctx *ctx, vs_kstat *velocity_cg, vs_kstat *simple_cg,
                     int64_t *total_kernel_launches);
 
+/* Debug: with VOXSCHUR_PHASE_TIMING set at context creation, the summed
+ * %globaltimer nanoseconds block 0 spent in {P1 pass, reduction 1, P2
+ * pass, reduction 2} since the last call (then reset); zeros otherwise. */
+int vs_phase_timing(vs_ctx *ctx, double *ns4);
+
 #ifdef __cplusplus
 }
 #endif

@@ -89,6 +89,7 @@ def _load():
         "vs_solve_schur": (C.c_int, [P, C.POINTER(VsSchurCfg), P, P, C.POINTER(VsReport),
                                      P, P, P, P, P]),
         "vs_kernel_stats": (C.c_int, [P, C.POINTER(VsKstat), C.POINTER(VsKstat), i64p]),
+        "vs_phase_timing": (C.c_int, [P, dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)  # AttributeError here = the ABI is incomplete
@@ -103,6 +104,7 @@ EXPORTED = (
     "vs_counts", "vs_export_geometry", "vs_apply_laplacian", "vs_apply_divergence",
     "vs_apply_gradient", "vs_divergence_weighted_diagonal", "vs_apply_simple",
     "vs_solve_velocity", "vs_solve_simple", "vs_solve_schur", "vs_kernel_stats",
+    "vs_phase_timing",
 )
 
 

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -75,11 +76,12 @@ struct vs_ctx {
     // pressure work vectors
     double *p_x, *p_r, *p_d, *p_z, *p_q, *p_b, *p_sr, *p_sz, *p_sd0, *p_sd1, *p_tmp;
     unsigned *bar = nullptr;
+    unsigned long long *phase_ns = nullptr;  // VOXSCHUR_PHASE_TIMING=1
     double *part = nullptr, *red_part = nullptr, *scal = nullptr;
     CgOut *cgout = nullptr;
     double *h_scal = nullptr;  // pinned
     CgOut *h_cg = nullptr;     // pinned
-    int grid_A = 0, grid_S = 0;
+    CgPlan plan_A{}, plan_S{};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
     // stats of the last top-level call
     vs_kstat st_A{}, st_S{};
@@ -223,6 +225,7 @@ int64_t cg_solve(vs_ctx *c, int op, const double *rhs, const double *x0, double 
     P.r = op == 0 ? c->u_r : c->p_sr;
     P.z = op == 0 ? c->u_z : c->p_sz;
     P.bar = c->bar;
+    P.phase_ns = c->phase_ns;
     P.d0 = op == 0 ? c->u_d0 : c->p_sd0;
     P.d1 = op == 0 ? c->u_d1 : c->p_sd1;
     P.part = c->part;
@@ -236,10 +239,11 @@ int64_t cg_solve(vs_ctx *c, int op, const double *rhs, const double *x0, double 
     memcpy(P.inv_code, c->inv_code, sizeof P.inv_code);
     memcpy(P.invA_enc, c->invA_enc, sizeof P.invA_enc);
     P.invS = c->invS;
-    const int gmax = op == 0 ? c->grid_A : c->grid_S;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (m + CG_THREADS - 1) / CG_THREADS));
+    const CgPlan &pl = op == 0 ? c->plan_A : c->plan_S;
+    CK(cudaMemsetAsync(c->bar, 0, sizeof(unsigned), c->stream));
+    ++c->launches;
     CK(cudaEventRecord(c->evs0, c->stream));
-    CK(launch_pcg(c->dim, op, P, grid, c->stream));
+    CK(launch_pcg(c->dim, op, pl, P, c->stream));
     CK(cudaEventRecord(c->evs1, c->stream));
     ++c->launches;
     CK(cudaMemcpyAsync(c->h_cg, c->cgout, sizeof(CgOut), cudaMemcpyDeviceToHost, c->stream));
@@ -482,11 +486,15 @@ int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_
         for (double **v : {&C->p_x, &C->p_r, &C->p_d, &C->p_z, &C->p_q, &C->p_b, &C->p_sr, &C->p_sz, &C->p_sd0,
                            &C->p_sd1, &C->p_tmp})
             *v = C->alloc<double>(mp);
-        C->grid_A = pcg_max_grid(dim, 0, device);
-        C->grid_S = pcg_max_grid(dim, 1, device);
+        C->plan_A = pcg_plan(dim, 0, C->m_u, device);
+        C->plan_S = pcg_plan(dim, 1, C->m_p, device);
         C->bar = C->alloc<unsigned>(2);
+        if (getenv("VOXSCHUR_PHASE_TIMING")) {
+            C->phase_ns = C->alloc<unsigned long long>(4);
+            CK(cudaMemsetAsync(C->phase_ns, 0, 4 * sizeof(unsigned long long), C->stream));
+        }
         CK(cudaMemsetAsync(C->bar, 0, 2 * sizeof(unsigned), C->stream));
-        C->part = C->alloc<double>((size_t)4 * 8 * std::max(C->grid_A, C->grid_S));
+        C->part = C->alloc<double>((size_t)4 * 8 * std::max(C->plan_A.grid, C->plan_S.grid));
         C->red_part = C->alloc<double>(RED_MAX_BLOCKS);
         C->scal = C->alloc<double>(8);
         C->cgout = C->alloc<CgOut>(1);
@@ -708,6 +716,18 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
         put(perm_history, ph);
         put(alpha_out, al);
         put(beta_out, be);
+    });
+}
+
+int vs_phase_timing(vs_ctx *c, double *ns4) {
+    return guarded(c, [&] {
+        unsigned long long h[4] = {0, 0, 0, 0};
+        if (c->phase_ns) {
+            CK(cudaMemcpyAsync(h, c->phase_ns, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemsetAsync(c->phase_ns, 0, sizeof h, c->stream));
+            c->sync();
+        }
+        for (int k = 0; k < 4; ++k) ns4[k] = (double)h[k];
     });
 }
 

@@ -96,6 +96,16 @@ __device__ __forceinline__ const uint2 *family_meta(const CgParams &P, uint64_t 
     return c == 0 ? P.g.vmeta[0] : (c == 1 ? P.g.vmeta[1] : P.g.vmeta[2]);
 }
 
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // ------------------------------------------------------------- grid barrier
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     unsigned v;
@@ -106,29 +116,29 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// bar[0] = arrival count, bar[1] = generation.  All blocks co-resident
-// (cooperative launch).  The last arriver resets the count and bumps the
-// generation; everyone else polls the generation with acquire loads.
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
+// bar[0] = monotonic arrival counter, zeroed by the host before each launch.
+// Barrier number b (1-based) completes when the counter reaches b*gridDim.x:
+// one red.release per block, then thread 0 polls with acquire loads.
+// (Measured on B200: ~1.2-1.4 us per barrier for 148-296 blocks, the same
+// as cooperative_groups grid.sync; tools/gridsync_micro.cu.)
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target) {
     __syncthreads();
+    target += gridDim.x;
     if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned old = atomicAdd(bar, 1u);
-        if (old == gridDim.x - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            st_release(bar + 1, gen + 1);
-        } else {
-            while (ld_acquire(bar + 1) == gen) {
-            }
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        while ((int)(ld_acquire(bar) - target) < 0) {
         }
     }
-    ++gen;
     __syncthreads();
 }
 
+// Deterministic grid-wide sum of K values.  Each block writes its K block
+// sums block-major (part[b*8 + k]); after the barrier every block reads ALL
+// block sums in one parallel round trip (thread t <- block t) and reduces
+// them in the same fixed tree, so every block obtains bitwise-identical
+// totals (no serial chain of dependent L2 loads).
 template <int K>
-__device__ __forceinline__ void grid_sum(double (&v)[K], double *part, unsigned *bar, unsigned &gen,
+__device__ __forceinline__ void grid_sum(double (&v)[K], double *part, unsigned *bar, unsigned &target,
                                          double (*s_warp)[5], double *s_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -143,30 +153,85 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], double *part, unsigned 
         double s = 0.0;
 #pragma unroll
         for (int w = 0; w < CG_THREADS / 32; ++w) s = __dadd_rn(s, s_warp[w][threadIdx.x]);
-        part[threadIdx.x * gridDim.x + blockIdx.x] = s;
+        part[blockIdx.x * 8 + threadIdx.x] = s;
     }
-    grid_barrier(bar, gen);
-    if (warp == 0) {
+    grid_barrier(bar, target);
+    double t[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double s = 0.0;
-            for (int j = lane; j < (int)gridDim.x; j += 32) s = __dadd_rn(s, __ldcg(part + k * gridDim.x + j));
+    for (int k = 0; k < K; ++k) t[k] = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += CG_THREADS) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(~0u, s, o));
-            if (lane == 0) s_tot[k] = s;
-        }
+        for (int k = 0; k < K; ++k) t[k] = __dadd_rn(t[k], __ldcg(part + b * 8 + k));
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double x = t[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(~0u, x, o));
+        t[k] = x;
+    }
+    __syncthreads();  // s_warp reuse
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) s_warp[warp][k] = t[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < CG_THREADS / 32; ++w) s = __dadd_rn(s, s_warp[w][threadIdx.x]);
+        s_tot[threadIdx.x] = s;
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = s_tot[k];
-    __syncthreads();
 }
 
 // ------------------------------------------------------------------ kernel
-template <int DIM, int OP>
+// Block-resident DOF cache: a persistent block visits the same DOFs every
+// iteration (i = tid + k*stride), so slot k of thread t keeps, in shared
+// memory, the DOF's record (TIER >= 1) and its 2*DIM neighbour ranks
+// (TIER 2) for the first `kc` slots.  Cached DOFs skip the record read
+// (8 B/DOF/pass of DRAM) and, at TIER 2, the whole bitmask rank lookup.
+template <int DIM, int OP, int TIER>
+struct DofCache {
+    static constexpr int NS = 2 * DIM;
+    uint64_t *rec;
+    uint32_t *rank;
+    __device__ DofCache(uint8_t *base, uint32_t kc) {
+        rec = reinterpret_cast<uint64_t *>(base);
+        rank = reinterpret_cast<uint32_t *>(base + (size_t)kc * CG_THREADS * 8);
+    }
+    __device__ __forceinline__ void put(uint32_t k, uint64_t rc, const uint32_t (&nr)[NS]) {
+        rec[k * CG_THREADS + threadIdx.x] = rc;
+        if (TIER == 2) {
+#pragma unroll
+            for (int s = 0; s < NS; ++s) rank[(k * NS + s) * CG_THREADS + threadIdx.x] = nr[s];
+        }
+    }
+};
+
+template <int DIM, int OP, int TIER>
+__device__ __forceinline__ void fetch_dof(const CgParams &P, const DofCache<DIM, OP, TIER> &C, uint32_t k,
+                                          uint32_t kc, uint32_t i, uint64_t &rc, uint32_t (&nr)[2 * DIM]) {
+    if (k < kc) {
+        rc = C.rec[k * CG_THREADS + threadIdx.x];
+        if (TIER == 2) {
+#pragma unroll
+            for (int s = 0; s < 2 * DIM; ++s) nr[s] = C.rank[(k * 2 * DIM + s) * CG_THREADS + threadIdx.x];
+            return;
+        }
+    } else {
+        rc = P.rec[i];
+    }
+    neighbour_ranks<DIM>(family_meta<OP>(P, rc), P.g.nw, P.g.n, rc, nr);
+}
+
+template <int DIM, int OP, int TIER>
 __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
+    extern __shared__ __align__(16) uint8_t dyn_smem[];
     __shared__ double s_tab[40];
     __shared__ double s_warp[CG_THREADS / 32][5];
     __shared__ double s_tot[5];
@@ -175,18 +240,19 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
         s_tab[16 + threadIdx.x] = P.inv_code[threadIdx.x];
         if (threadIdx.x < 8) s_tab[32 + threadIdx.x] = P.invA_enc[threadIdx.x];
     }
-    unsigned gen = ld_acquire(P.bar + 1);
+    unsigned gen = 0;  // barrier target (counter zeroed by the host)
+    const uint32_t kc = P.cache_slots;
+    DofCache<DIM, OP, TIER> cache(dyn_smem, kc);
     __syncthreads();
     const Tabs T{s_tab, s_tab + 16, s_tab + 32, P.invS};
-    const int n = P.g.n, nw = P.g.nw;
     const uint32_t m = (uint32_t)P.m;
     const uint32_t tid = blockIdx.x * CG_THREADS + threadIdx.x;
     const uint32_t stride = gridDim.x * CG_THREADS;
-    const uint64_t *__restrict__ rec = P.rec;
     double *x = P.x, *r = P.r, *z = P.z;
     const double inv_h = P.inv_h, inv_h2 = P.inv_h2;
 
-    // ---- setup (krylov.py:102-119): project rhs; r = op(x0) - rhs; z = M^-1 r
+    // ---- setup (krylov.py:102-119): project rhs; r = op(x0) - rhs; z = M^-1 r;
+    //      fill the DOF cache
     double mu_rhs = 0.0, mu = 0.0, rz = 0.0, rp0 = 0.0, ru0 = 0.0;
     if (PROJ) {
         double v[1] = {0.0};
@@ -197,13 +263,15 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     {
         double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         const double *x0 = P.x0;
-        for (uint32_t i = tid; i < m; i += stride) {
-            const uint64_t rc = rec[i];
+        uint32_t k = 0;
+        for (uint32_t i = tid; i < m; i += stride, ++k) {
+            const uint64_t rc = P.rec[i];
+            uint32_t nr[NS];
+            if (x0 || (TIER == 2 && k < kc)) neighbour_ranks<DIM>(family_meta<OP>(P, rc), P.g.nw, P.g.n, rc, nr);
+            if (k < kc) cache.put(k, rc, nr);
             double ax = 0.0, xi = 0.0;
             if (x0) {
                 xi = x0[i];
-                uint32_t nr[NS];
-                neighbour_ranks<DIM>(family_meta<OP>(P, rc), nw, n, rc, nr);
                 double vn[NS];
 #pragma unroll
                 for (int s = 0; s < NS; ++s) vn[s] = nr[s] != ABSENT ? x0[nr[s]] : 0.0;
@@ -240,55 +308,76 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     bool conv = (ref == 0.0);
     double *dold = P.d0, *dnew = P.d1;
     if (!conv) {
-        for (int64_t k = 0; k < P.max_iter; ++k) {
-            if (rz < 0.0) { status = 1; sval = rz; sat = k; break; }
+        for (int64_t it = 0; it < P.max_iter; ++it) {
+            if (rz < 0.0) { status = 1; sval = rz; sat = it; break; }
             if (rz == 0.0) { conv = true; break; }
-            const bool first = (k == 0);
+            const bool first = (it == 0);
+            const uint64_t t0 = P.phase_ns ? gtimer() : 0;
             // ---- P1: d = z - mu + beta d_old, q = op(d), d.q
             double v1[1] = {0.0};
-            uint64_t rc_next = tid < m ? rec[tid] : 0;
-            for (uint32_t i = tid; i < m; i += stride) {
-                const uint64_t rc = rc_next;
-                if (i + stride < m) rc_next = rec[i + stride];
-                uint32_t nr[NS];
-                neighbour_ranks<DIM>(family_meta<OP>(P, rc), nw, n, rc, nr);
+            uint32_t k = 0;
+            for (uint32_t i = tid; i < m; i += stride, ++k) {
+                const uint32_t ip = i + 2 * stride;
+                if (ip < m) {  // stream the centre vectors two strides ahead
+                    if (k + 2 >= kc) prefetch_l2(P.rec + ip);
+                    prefetch_l2(z + ip);
+                    if (!first) prefetch_l2(dold + ip);
+                }
                 double zc = z[i];
+                const double dc = first ? 0.0 : dold[i];
+                uint64_t rc;
+                uint32_t nr[NS];
+                fetch_dof<DIM, OP, TIER>(P, cache, k, kc, i, rc, nr);
+                double zn[NS], dn[NS];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {  // unconditional loads (absent -> own index)
+                    const uint32_t j = nr[s] != ABSENT ? nr[s] : i;
+                    zn[s] = z[j];
+                    dn[s] = first ? 0.0 : dold[j];
+                }
                 if (PROJ) zc = __dsub_rn(zc, mu);
-                const double di = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dold[i]));
+                const double di = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dc));
                 double vn[NS];
 #pragma unroll
                 for (int s = 0; s < NS; ++s) {
-                    double zj = 0.0, dj = 0.0;
-                    if (nr[s] != ABSENT) {
-                        zj = z[nr[s]];
-                        if (!first) dj = dold[nr[s]];
-                    }
+                    double zj = zn[s];
                     if (PROJ) zj = __dsub_rn(zj, mu);
-                    vn[s] = nr[s] == ABSENT ? 0.0 : (first ? zj : __dadd_rn(zj, __dmul_rn(beta, dj)));
+                    const double dj = first ? zj : __dadd_rn(zj, __dmul_rn(beta, dn[s]));
+                    vn[s] = nr[s] == ABSENT ? 0.0 : dj;
                 }
                 const double qi = op_value<DIM, OP>(rc, di, vn, T, inv_h, inv_h2);
                 dnew[i] = di;
                 v1[0] = __dadd_rn(v1[0], __dmul_rn(di, qi));
             }
+            const uint64_t t1 = P.phase_ns ? gtimer() : 0;
             grid_sum<1>(v1, P.part + 16 * gridDim.x, P.bar, gen, s_warp, s_tot);
+            const uint64_t t2 = P.phase_ns ? gtimer() : 0;
             const double dq = v1[0];
-            if (dq <= 0.0) { status = 2; sval = dq; sat = k; break; }
+            if (dq <= 0.0) { status = 2; sval = dq; sat = it; break; }
             const double alpha = rz / dq;
             // ---- P2: q = op(d); x -= alpha d; r -= alpha q; z = M^-1 r; sums
             double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            rc_next = tid < m ? rec[tid] : 0;
-            for (uint32_t i = tid; i < m; i += stride) {
-                const uint64_t rc = rc_next;
-                if (i + stride < m) rc_next = rec[i + stride];
+            k = 0;
+            for (uint32_t i = tid; i < m; i += stride, ++k) {
+                const uint32_t ip = i + 2 * stride;
+                if (ip < m) {
+                    if (k + 2 >= kc) prefetch_l2(P.rec + ip);
+                    prefetch_l2(dnew + ip);
+                    prefetch_l2(x + ip);
+                    prefetch_l2(r + ip);
+                }
+                const double di = dnew[i], xo = x[i], ro = r[i];
+                uint64_t rc;
                 uint32_t nr[NS];
-                neighbour_ranks<DIM>(family_meta<OP>(P, rc), nw, n, rc, nr);
+                fetch_dof<DIM, OP, TIER>(P, cache, k, kc, i, rc, nr);
                 double vn[NS];
 #pragma unroll
-                for (int s = 0; s < NS; ++s) vn[s] = nr[s] != ABSENT ? dnew[nr[s]] : 0.0;
-                const double di = dnew[i];
+                for (int s = 0; s < NS; ++s) vn[s] = dnew[nr[s] != ABSENT ? nr[s] : i];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) vn[s] = nr[s] == ABSENT ? 0.0 : vn[s];
                 const double qi = op_value<DIM, OP>(rc, di, vn, T, inv_h, inv_h2);
-                const double xi = __dsub_rn(x[i], __dmul_rn(alpha, di));
-                const double ri = __dsub_rn(r[i], __dmul_rn(alpha, qi));
+                const double xi = __dsub_rn(xo, __dmul_rn(alpha, di));
+                const double ri = __dsub_rn(ro, __dmul_rn(alpha, qi));
                 const double zi = __dmul_rn(ri, jacobi_inv<OP>(rc, T));
                 x[i] = xi;
                 r[i] = ri;
@@ -299,7 +388,15 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
                 v[3] = __dadd_rn(v[3], zi);
                 v[4] = __dadd_rn(v[4], ri);
             }
+            const uint64_t t3 = P.phase_ns ? gtimer() : 0;
             grid_sum<5>(v, P.part + 24 * gridDim.x, P.bar, gen, s_warp, s_tot);
+            if (P.phase_ns && blockIdx.x == 0 && threadIdx.x == 0) {
+                const uint64_t t4 = gtimer();
+                P.phase_ns[0] += t1 - t0;
+                P.phase_ns[1] += t2 - t1;
+                P.phase_ns[2] += t3 - t2;
+                P.phase_ns[3] += t4 - t3;
+            }
             if (PROJ) {
                 mu = v[3] / (double)P.m;
                 v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
@@ -309,8 +406,8 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
             beta = rz_new / rz;
             rz = rz_new;
             const double nz = sqrt(v[1]), nrr = sqrt(v[2]);
-            if (!(isfinite(nz) && isfinite(nrr))) { status = 3; sat = k + 1; break; }
-            its = k + 1;
+            if (!(isfinite(nz) && isfinite(nrr))) { status = 3; sat = it + 1; break; }
+            its = it + 1;
             rp_last = nz;
             ru_last = nrr;
             double *t = dold; dold = dnew; dnew = t;
@@ -331,21 +428,47 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     }
 }
 
-static const void *pcg_fn(int dim, int op) {
-    if (dim == 3) return op == 0 ? (const void *)k_pcg<3, 0> : (const void *)k_pcg<3, 1>;
-    return op == 0 ? (const void *)k_pcg<2, 0> : (const void *)k_pcg<2, 1>;
+template <int DIM, int OP>
+static const void *pcg_fn_t(int tier) {
+    return tier == 2 ? (const void *)k_pcg<DIM, OP, 2> : (const void *)k_pcg<DIM, OP, 1>;
+}
+static const void *pcg_fn(int dim, int op, int tier) {
+    if (dim == 3) return op == 0 ? pcg_fn_t<3, 0>(tier) : pcg_fn_t<3, 1>(tier);
+    return op == 0 ? pcg_fn_t<2, 0>(tier) : pcg_fn_t<2, 1>(tier);
 }
 
-int pcg_max_grid(int dim, int op, int device) {
-    int per_sm = 0, nsm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_fn(dim, op), CG_THREADS, 0);
+// Plan one launch: grid (co-resident blocks), cache tier and slots, smem.
+CgPlan pcg_plan(int dim, int op, int64_t m, int device) {
+    CgPlan pl{};
+    int nsm = 0, maxopt = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    return per_sm * nsm;
+    cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    const int ns = 2 * dim;
+    const size_t budget = std::min<size_t>(CG_SMEM_BUDGET, (size_t)maxopt);
+    for (int tier = 2; tier >= 1; --tier) {
+        const void *fn = pcg_fn(dim, op, tier);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CG_THREADS, budget);
+        if (per_sm < 1) per_sm = 1;
+        int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * nsm, (m + CG_THREADS - 1) / CG_THREADS));
+        const int64_t stride = (int64_t)grid * CG_THREADS;
+        const int64_t slots = (m + stride - 1) / stride;
+        const size_t per_slot = (size_t)CG_THREADS * (tier == 2 ? 8 + 4 * ns : 8);
+        if (tier == 2 && (size_t)slots * per_slot > budget) continue;
+        pl.tier = tier;
+        pl.grid = grid;
+        pl.slots = (uint32_t)std::min<int64_t>(slots, (int64_t)(budget / per_slot));
+        pl.smem = pl.slots * per_slot;
+        return pl;
+    }
+    return pl;
 }
 
-cudaError_t launch_pcg(int dim, int op, CgParams &P, int grid, cudaStream_t s) {
+cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, CgParams &P, cudaStream_t s) {
+    P.cache_slots = pl.slots;
     void *args[] = {&P};
-    return cudaLaunchCooperativeKernel(pcg_fn(dim, op), dim3(grid), dim3(CG_THREADS), args, 0, s);
+    return cudaLaunchCooperativeKernel(pcg_fn(dim, op, pl.tier), dim3(pl.grid), dim3(CG_THREADS), args, pl.smem, s);
 }
 
 }  // namespace vs

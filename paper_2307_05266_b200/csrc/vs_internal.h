@@ -1,5 +1,6 @@
 // vs_internal.h -- host-side declarations shared by the API and the kernels.
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -27,7 +28,9 @@ struct CgParams {
     const double *rhs, *x0;
     double *x, *r, *z, *d0, *d1;
     double *part;  // 4 sets x 8 slots x grid
-    unsigned *bar; // grid barrier {count, generation}
+    unsigned *bar; // grid barrier counter
+    uint32_t cache_slots;
+    unsigned long long *phase_ns;  // optional [4] accumulators (block 0): P1, sum1, P2, sum2
     CgOut *out;
     double tol;
     int64_t max_iter;
@@ -64,7 +67,13 @@ void launch_vec(int kind, double *out, double *a, const double *b, double sc, in
 void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s);
 int launch_reduce(int kind, const double *a, const double *b, int64_t m, double *part, double *out,
                   cudaStream_t s);
-int pcg_max_grid(int dim, int op, int device);
-cudaError_t launch_pcg(int dim, int op, CgParams &P, int grid, cudaStream_t s);
+constexpr size_t CG_SMEM_BUDGET = 108 * 1024;  // dynamic smem per block (2 blocks / SM)
+struct CgPlan {
+    int tier, grid;
+    uint32_t slots;
+    size_t smem;
+};
+CgPlan pcg_plan(int dim, int op, int64_t m, int device);
+cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, CgParams &P, cudaStream_t s);
 
 }  // namespace vs

@@ -7,7 +7,9 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("VOXSCHUR_PHASE_TIMING", "1")
 import paper_2307_05266_b200 as vx  # noqa: E402
+from paper_2307_05266_b200 import _lib  # noqa: E402
 from paper_2307_05266_b200 import configs, schur  # noqa: E402
 
 key = sys.argv[1] if len(sys.argv) > 1 else "C1"
@@ -22,10 +24,15 @@ rhs_u = s.apply_gradient(p)
 for _ in range(reps):
     x, its = schur._solve_velocity(s, rhs_u, 1e-12)
     st = vx.last_kernel_stats(s)["velocity_cg"]
+    ph = np.zeros(4)
+    _lib.lib.vs_phase_timing(s._ctx, ph)
+    print("   phases us/it (P1, sum1, P2, sum2):", np.round(ph / its / 1e3, 2))
     print(f"A-solve: {its} its, {st['ms']:.3f} ms, {1e3 * st['ms'] / its:.2f} us/it, "
           f"{64 * st['dof_iters'] / st['ms'] / 1e6:.1f} GB/s alg", flush=True)
     z = vx.apply_simple_inverse(s, p, 1e-12)
     st = vx.last_kernel_stats(s)["simple_cg"]
     its = st["iterations"]
+    _lib.lib.vs_phase_timing(s._ctx, ph)
+    print("   phases us/it (P1, sum1, P2, sum2):", np.round(ph / its / 1e3, 2))
     print(f"S-solve: {its} its, {st['ms']:.3f} ms, {1e3 * st['ms'] / its:.2f} us/it, "
           f"{64 * st['dof_iters'] / st['ms'] / 1e6:.1f} GB/s alg", flush=True)
