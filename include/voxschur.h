@@ -134,10 +134,11 @@ typedef struct {
 int vs_kernel_stats(vs_ctx *ctx, vs_kstat *velocity_cg, vs_kstat *simple_cg,
                     int64_t *total_kernel_launches);
 
-/* Debug: with VOXSCHUR_PHASE_TIMING set at context creation, the summed
- * %globaltimer nanoseconds block 0 spent in {P1 pass, reduction 1, P2
- * pass, reduction 2} since the last call (then reset); zeros otherwise. */
-int vs_phase_timing(vs_ctx *ctx, double *ns4);
+/* Debug: with VOXSCHUR_PHASE_TIMING set at context creation, %globaltimer
+ * nanoseconds spent in {P1 pass, reduction 1, P2 pass, reduction 2} since
+ * the last call (then reset): ns12[0..3] block 0, [4..7] max over blocks,
+ * [8..11] sum over blocks.  Zeros otherwise. */
+int vs_phase_timing(vs_ctx *ctx, double *ns12);
 
 #ifdef __cplusplus
 }

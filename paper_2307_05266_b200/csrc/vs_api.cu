@@ -490,8 +490,8 @@ int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_
         C->plan_S = pcg_plan(dim, 1, C->m_p, device);
         C->bar = C->alloc<unsigned>(2);
         if (getenv("VOXSCHUR_PHASE_TIMING")) {
-            C->phase_ns = C->alloc<unsigned long long>(4);
-            CK(cudaMemsetAsync(C->phase_ns, 0, 4 * sizeof(unsigned long long), C->stream));
+            C->phase_ns = C->alloc<unsigned long long>(12);
+            CK(cudaMemsetAsync(C->phase_ns, 0, 12 * sizeof(unsigned long long), C->stream));
         }
         CK(cudaMemsetAsync(C->bar, 0, 2 * sizeof(unsigned), C->stream));
         C->part = C->alloc<double>((size_t)4 * 8 * std::max(C->plan_A.grid, C->plan_S.grid));
@@ -721,13 +721,13 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
 
 int vs_phase_timing(vs_ctx *c, double *ns4) {
     return guarded(c, [&] {
-        unsigned long long h[4] = {0, 0, 0, 0};
+        unsigned long long h[12] = {0};
         if (c->phase_ns) {
             CK(cudaMemcpyAsync(h, c->phase_ns, sizeof h, cudaMemcpyDeviceToHost, c->stream));
             CK(cudaMemsetAsync(c->phase_ns, 0, sizeof h, c->stream));
             c->sync();
         }
-        for (int k = 0; k < 4; ++k) ns4[k] = (double)h[k];
+        for (int k = 0; k < 12; ++k) ns4[k] = (double)h[k];
     });
 }
 

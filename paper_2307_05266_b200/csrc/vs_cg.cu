@@ -132,6 +132,31 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target) {
     __syncthreads();
 }
 
+// Warp 0 combines the per-warp values s_warp[w][k] (w < CG_THREADS/32) with
+// one xor-butterfly carrying all K values at once; the result lands in
+// every lane of warp 0.  Fixed shape -> bitwise identical in every block.
+template <int K>
+__device__ __forceinline__ void warp0_combine(const double (*s_warp)[5], double (&t)[K]) {
+    constexpr int NW = CG_THREADS / 32;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < K; ++k) t[k] = lane < NW ? s_warp[lane][k] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) t[k] = __dadd_rn(t[k], __shfl_xor_sync(~0u, t[k], o));
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void warp_tree(double (&t)[K]) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) t[k] = __dadd_rn(t[k], __shfl_xor_sync(~0u, t[k], o));
+    }
+}
+
 // Deterministic grid-wide sum of K values.  Each block writes its K block
 // sums block-major (part[b*8 + k]); after the barrier every block reads ALL
 // block sums in one parallel round trip (thread t <- block t) and reduces
@@ -141,21 +166,21 @@ template <int K>
 __device__ __forceinline__ void grid_sum(double (&v)[K], double *part, unsigned *bar, unsigned &target,
                                          double (*s_warp)[5], double *s_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    warp_tree<K>(v);
+    if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        double x = v[k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(~0u, x, o));
-        if (lane == 0) s_warp[warp][k] = x;
+        for (int k = 0; k < K; ++k) s_warp[warp][k] = v[k];
     }
     __syncthreads();
-    if (threadIdx.x < K) {
-        double s = 0.0;
+    if (warp == 0) {
+        double t[K];
+        warp0_combine<K>(s_warp, t);
+        if (lane == 0) {
 #pragma unroll
-        for (int w = 0; w < CG_THREADS / 32; ++w) s = __dadd_rn(s, s_warp[w][threadIdx.x]);
-        part[blockIdx.x * 8 + threadIdx.x] = s;
+            for (int k = 0; k < K; ++k) part[blockIdx.x * 8 + k] = t[k];
+        }
     }
-    grid_barrier(bar, target);
+    grid_barrier(bar, target);  // starts with __syncthreads (s_warp reuse is safe)
     double t[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) t[k] = 0.0;
@@ -163,24 +188,18 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], double *part, unsigned 
 #pragma unroll
         for (int k = 0; k < K; ++k) t[k] = __dadd_rn(t[k], __ldcg(part + b * 8 + k));
     }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        double x = t[k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(~0u, x, o));
-        t[k] = x;
-    }
-    __syncthreads();  // s_warp reuse
+    warp_tree<K>(t);
     if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < K; ++k) s_warp[warp][k] = t[k];
     }
     __syncthreads();
-    if (threadIdx.x < K) {
-        double s = 0.0;
+    if (warp == 0) {
+        warp0_combine<K>(s_warp, t);
+        if (lane == 0) {
 #pragma unroll
-        for (int w = 0; w < CG_THREADS / 32; ++w) s = __dadd_rn(s, s_warp[w][threadIdx.x]);
-        s_tot[threadIdx.x] = s;
+            for (int k = 0; k < K; ++k) s_tot[k] = t[k];
+        }
     }
     __syncthreads();
 #pragma unroll
@@ -307,6 +326,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     int64_t sat = 0, its = 0;
     bool conv = (ref == 0.0);
     double *dold = P.d0, *dnew = P.d1;
+    unsigned long long ph[4] = {0, 0, 0, 0};  // this block's phase sums (thread 0)
     if (!conv) {
         for (int64_t it = 0; it < P.max_iter; ++it) {
             if (rz < 0.0) { status = 1; sval = rz; sat = it; break; }
@@ -390,12 +410,12 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
             }
             const uint64_t t3 = P.phase_ns ? gtimer() : 0;
             grid_sum<5>(v, P.part + 24 * gridDim.x, P.bar, gen, s_warp, s_tot);
-            if (P.phase_ns && blockIdx.x == 0 && threadIdx.x == 0) {
+            if (P.phase_ns && threadIdx.x == 0) {
                 const uint64_t t4 = gtimer();
-                P.phase_ns[0] += t1 - t0;
-                P.phase_ns[1] += t2 - t1;
-                P.phase_ns[2] += t3 - t2;
-                P.phase_ns[3] += t4 - t3;
+                ph[0] += t1 - t0;
+                ph[1] += t2 - t1;
+                ph[2] += t3 - t2;
+                ph[3] += t4 - t3;
             }
             if (PROJ) {
                 mu = v[3] / (double)P.m;
@@ -412,6 +432,14 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
             ru_last = nrr;
             double *t = dold; dold = dnew; dnew = t;
             if ((P.norm_prec ? nz : nrr) / ref < P.tol) { conv = true; break; }
+        }
+    }
+    if (P.phase_ns && threadIdx.x == 0) {  // [0..3] block 0, [4..7] max, [8..11] sum over blocks
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            if (blockIdx.x == 0) P.phase_ns[p] += ph[p];
+            atomicMax(P.phase_ns + 4 + p, ph[p]);
+            atomicAdd(P.phase_ns + 8 + p, ph[p]);
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {

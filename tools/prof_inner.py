@@ -24,15 +24,18 @@ rhs_u = s.apply_gradient(p)
 for _ in range(reps):
     x, its = schur._solve_velocity(s, rhs_u, 1e-12)
     st = vx.last_kernel_stats(s)["velocity_cg"]
-    ph = np.zeros(4)
+    ph = np.zeros(12)
     _lib.lib.vs_phase_timing(s._ctx, ph)
-    print("   phases us/it (P1, sum1, P2, sum2):", np.round(ph / its / 1e3, 2))
+    grid = {"A": None}
+    print("   phases us/it (P1, sum1, P2, sum2) block0:", np.round(ph[:4] / its / 1e3, 2),
+          "max-block:", np.round(ph[4:8] / its / 1e3, 2))
     print(f"A-solve: {its} its, {st['ms']:.3f} ms, {1e3 * st['ms'] / its:.2f} us/it, "
           f"{64 * st['dof_iters'] / st['ms'] / 1e6:.1f} GB/s alg", flush=True)
     z = vx.apply_simple_inverse(s, p, 1e-12)
     st = vx.last_kernel_stats(s)["simple_cg"]
     its = st["iterations"]
     _lib.lib.vs_phase_timing(s._ctx, ph)
-    print("   phases us/it (P1, sum1, P2, sum2):", np.round(ph / its / 1e3, 2))
+    print("   phases us/it (P1, sum1, P2, sum2) block0:", np.round(ph[:4] / its / 1e3, 2),
+          "max-block:", np.round(ph[4:8] / its / 1e3, 2))
     print(f"S-solve: {its} its, {st['ms']:.3f} ms, {1e3 * st['ms'] / its:.2f} us/it, "
           f"{64 * st['dof_iters'] / st['ms'] / 1e6:.1f} GB/s alg", flush=True)
