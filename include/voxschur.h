@@ -88,6 +88,17 @@ int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir,
                   double inv_h, double inv_h2, vs_ctx **out);
 void vs_ctx_destroy(vs_ctx *ctx);
 
+/* As vs_ctx_create, decomposed into `slabs` x-slabs (1..16, <= n): slab s
+ * owns reference x-planes [s*n/slabs, (s+1)*n/slabs) plus one ghost plane
+ * per side; the fused inner PCG runs all slabs as groups of one cooperative
+ * grid that exchange z ghost planes every iteration and reduce in a fixed
+ * slab-major order.  On one GPU this emulates a multi-GPU run of `slabs`
+ * ranks (same kernel, same halo/reduction schedule). */
+int vs_ctx_create2(const uint8_t *fluid, int dim, int n, int flow_dir,
+                   int check_connectivity, int require_walls, int device,
+                   double inv_h, double inv_h2, int slabs, vs_ctx **out);
+int vs_slab_count(vs_ctx *ctx);
+
 /* DofMap sizes (operators.py:233-235, :247). */
 int vs_counts(vs_ctx *ctx, int64_t *m_u, int64_t *m_p, int64_t axis_counts[3]);
 

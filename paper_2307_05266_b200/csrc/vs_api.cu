@@ -55,26 +55,53 @@ struct Status {
 
 }  // namespace
 
+namespace {
+
+// ----------------------------------------------------------------- slabs
+// Vector slots of a slab.  Velocity slots have m_all[0] entries, pressure
+// slots m_all[1]; owned DOFs first, ghost-plane DOFs after.
+enum USlot { U_RHS, U_W, U_ITER, U_F, U_R, U_Z, U_D0, U_D1, U_TMP, U_IN, NU };
+enum PSlot { P_X, P_R, P_D, P_Z, P_Q, P_B, P_SR, P_SZ, P_SD0, P_SD1, P_TMP, P_IN, NP };
+constexpr int FP = 3;  // family index of the pressure (velocity components are 0..dim-1)
+
+// One group of the decomposition: a slab of x-planes [x_lo, x_hi) with one
+// ghost plane on each side.  With a single group it is the whole periodic
+// domain (nx = n, no ghosts, local numbering == reference numbering).
+struct Slab {
+    int x_lo = 0, x_hi = 0, P = 0, nx = 0;
+    int64_t own[4] = {0, 0, 0, 0}, own_off[4] = {0, 0, 0, 0};
+    int64_t glo_off[4] = {0, 0, 0, 0}, glo_cnt[4] = {0, 0, 0, 0};
+    int64_t ghi_off[4] = {0, 0, 0, 0}, ghi_cnt[4] = {0, 0, 0, 0};
+    int64_t first_cnt[4] = {0, 0, 0, 0}, last_cnt[4] = {0, 0, 0, 0};
+    int64_t gstart[4] = {0, 0, 0, 0};  // global rank of the first owned DOF per family
+    int64_t m_own[2] = {0, 0}, m_all[2] = {0, 0};
+    uint2 *meta[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint64_t *vrec = nullptr, *prec = nullptr;
+    double *u[NU] = {}, *p[NP] = {};
+    Geo geo{};
+};
+
+}  // namespace
+
 struct vs_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    int dim = 0, n = 0, nw = 0, nlines = 0, flow_dir = 0;
+    int dim = 0, n = 0, nw = 0, nlines = 0, flow_dir = 0, R = 1;
     int64_t nwords = 0, ncells = 0;
     int64_t m_u = 0, m_p = 0, vcount[3] = {0, 0, 0}, voff[3] = {0, 0, 0};
     double inv_h = 0, inv_h2 = 0, diag_scale = 0;
     double diag_code[16] = {0}, inv_code[16] = {0}, invA_enc[8] = {0};
     bool sdiag_ok = true;
     std::vector<void *> allocs;
-    // geometry
+    // global geometry (reference numbering)
     uint32_t *fbits = nullptr;
     uint2 *vmeta[3] = {nullptr, nullptr, nullptr};
     uint2 *pmeta = nullptr;
     uint64_t *vrec = nullptr, *prec = nullptr;
     double *invS = nullptr, *d_diag_code = nullptr, *d_invA_enc = nullptr;
-    // velocity work vectors
-    double *u_rhs, *u_w, *u_iter, *u_f, *u_r, *u_z, *u_d0, *u_d1, *u_tmp;
-    // pressure work vectors
-    double *p_x, *p_r, *p_d, *p_z, *p_q, *p_b, *p_sr, *p_sz, *p_sd0, *p_sd1, *p_tmp;
+    std::vector<int64_t> pstart[4];  // global rank of the first DOF of plane x, x in [0, n]
+    std::vector<Slab> slabs;
+    CgGroup *d_groups = nullptr, *h_groups = nullptr;  // [R] device / pinned staging
     unsigned *bar = nullptr;
     unsigned long long *phase_ns = nullptr;  // VOXSCHUR_PHASE_TIMING=1
     double *part = nullptr, *red_part = nullptr, *scal = nullptr;
@@ -83,13 +110,12 @@ struct vs_ctx {
     CgOut *h_cg = nullptr;     // pinned
     CgPlan plan_A{}, plan_S{};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
-    // stats of the last top-level call
-    vs_kstat st_A{}, st_S{};
+    vs_kstat st_A{}, st_S{};  // stats of the last top-level call
     int64_t launches = 0;
 
     Geo geo() const {
         Geo g;
-        g.dim = dim; g.n = n; g.nw = nw; g.nlines = nlines;
+        g.dim = dim; g.n = n; g.nw = nw; g.nlines = nlines; g.nx = n;
         g.fbits = fbits;
         for (int a = 0; a < 3; ++a) g.vmeta[a] = vmeta[a];
         g.pmeta = pmeta;
@@ -107,25 +133,132 @@ struct vs_ctx {
         for (void *p : allocs) cudaFree(p);
         if (h_scal) cudaFreeHost(h_scal);
         if (h_cg) cudaFreeHost(h_cg);
+        if (h_groups) cudaFreeHost(h_groups);
         for (cudaEvent_t e : {ev0, ev1, evs0, evs1})
             if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
     }
     void sync() { CK(cudaStreamSynchronize(stream)); }
-    // deterministic device reduction, result on host
-    double reduce(int kind, const double *a, const double *b, int64_t m) {
-        if (m == 0) return 0.0;
-        launches += launch_reduce(kind, a, b, m, red_part, scal, stream);
-        CK(cudaMemcpyAsync(h_scal, scal, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    int nfam() const { return dim; }
+    // ---- distributed-vector helpers (loop over slabs, fixed order)
+    double *U(int s, int slot) { return slabs[s].u[slot]; }
+    double *Pv(int s, int slot) { return slabs[s].p[slot]; }
+    // deterministic reduction over the owned DOFs of every slab, result on host
+    double reduce(int space, int kind, int a, int b, int64_t lo_fam = -1) {
+        double tot = 0.0;
+        for (int s = 0; s < R; ++s) {
+            Slab &S = slabs[s];
+            const double *pa = space == 0 ? S.u[a] : S.p[a];
+            const double *pb = b < 0 ? nullptr : (space == 0 ? S.u[b] : S.p[b]);
+            int64_t off = 0, m = S.m_own[space];
+            if (lo_fam >= 0) { off = S.own_off[lo_fam]; m = S.own[lo_fam]; }
+            if (m == 0) continue;
+            launches += launch_reduce(kind, pa + off, pb ? pb + off : nullptr, m, red_part, scal + s, stream);
+        }
+        CK(cudaMemcpyAsync(h_scal, scal, R * sizeof(double), cudaMemcpyDeviceToHost, stream));
         sync();
-        return h_scal[0];
+        for (int s = 0; s < R; ++s) tot = (s == 0) ? h_scal[0] : tot + h_scal[s];
+        return tot;
     }
-    double dot(const double *a, const double *b, int64_t m) { return reduce(1, a, b, m); }
-    double sum(const double *a, int64_t m) { return reduce(0, a, nullptr, m); }
-    double mean(const double *a, int64_t m) { return sum(a, m) / (double)m; }
-    void vec(int kind, double *out, double *a, const double *b, double s, int64_t m) {
-        launch_vec(kind, out, a, b, s, m, stream);
-        ++launches;
+    double dot(int space, int a, int b) { return reduce(space, 1, a, b); }
+    double sum(int space, int a) { return reduce(space, 0, a, -1); }
+    double mean(int space, int a) { return sum(space, a) / (double)(space == 0 ? m_u : m_p); }
+    void vec(int space, int kind, int out, int a, int b, double sc) {
+        for (int s = 0; s < R; ++s) {
+            Slab &S = slabs[s];
+            double **v = space == 0 ? S.u : S.p;
+            launch_vec(kind, out < 0 ? nullptr : v[out], v[a], b < 0 ? nullptr : v[b], sc, S.m_own[space], stream);
+            ++launches;
+        }
+    }
+    void copy(int space, int dst, int src) {
+        for (int s = 0; s < R; ++s) {
+            Slab &S = slabs[s];
+            double **v = space == 0 ? S.u : S.p;
+            if (S.m_own[space])
+                CK(cudaMemcpyAsync(v[dst], v[src], S.m_own[space] * sizeof(double), cudaMemcpyDeviceToDevice,
+                                   stream));
+        }
+    }
+    // fill the ghost planes of a vector from the neighbouring slabs' owned
+    // boundary planes (device-to-device; peer copies on a multi-GPU run)
+    void halo(int space, int slot) {
+        if (R == 1) return;
+        for (int s = 0; s < R; ++s) {
+            Slab &S = slabs[s], &lo = slabs[(s - 1 + R) % R], &hi = slabs[(s + 1) % R];
+            const int nf = space == 0 ? dim : 1;
+            for (int k = 0; k < nf; ++k) {
+                const int f = space == 0 ? k : FP;
+                double *dst = space == 0 ? S.u[slot] : S.p[slot];
+                const double *slo = space == 0 ? lo.u[slot] : lo.p[slot];
+                const double *shi = space == 0 ? hi.u[slot] : hi.p[slot];
+                if (S.glo_cnt[f])
+                    CK(cudaMemcpyAsync(dst + S.glo_off[f], slo + lo.own_off[f] + lo.own[f] - lo.last_cnt[f],
+                                       S.glo_cnt[f] * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+                if (S.ghi_cnt[f])
+                    CK(cudaMemcpyAsync(dst + S.ghi_off[f], shi + hi.own_off[f], S.ghi_cnt[f] * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, stream));
+            }
+        }
+    }
+    // host (reference order) -> slabs, owned and ghost planes
+    void upload(int space, int slot, const double *h) {
+        for (int s = 0; s < R; ++s) {
+            Slab &S = slabs[s];
+            double *dst = space == 0 ? S.u[slot] : S.p[slot];
+            const int nf = space == 0 ? dim : 1;
+            for (int k = 0; k < nf; ++k) {
+                const int f = space == 0 ? k : FP;
+                auto put = [&](int64_t loff, int64_t goff, int64_t cnt) {
+                    if (cnt) CK(cudaMemcpyAsync(dst + loff, h + goff, cnt * sizeof(double), cudaMemcpyHostToDevice,
+                                                stream));
+                };
+                put(S.own_off[f], S.gstart[f], S.own[f]);
+                if (R > 1) {
+                    put(S.glo_off[f], pstart[f][(S.x_lo - 1 + n) % n], S.glo_cnt[f]);
+                    put(S.ghi_off[f], pstart[f][S.x_hi % n], S.ghi_cnt[f]);
+                }
+            }
+        }
+    }
+    void download(int space, int slot, double *h) {
+        if (!h) return;
+        for (int s = 0; s < R; ++s) {
+            Slab &S = slabs[s];
+            const double *src = space == 0 ? S.u[slot] : S.p[slot];
+            const int nf = space == 0 ? dim : 1;
+            for (int k = 0; k < nf; ++k) {
+                const int f = space == 0 ? k : FP;
+                if (S.own[f])
+                    CK(cudaMemcpyAsync(h + S.gstart[f], src + S.own_off[f], S.own[f] * sizeof(double),
+                                       cudaMemcpyDeviceToHost, stream));
+            }
+        }
+    }
+    // ---- outer operators on every slab (ghosts of the input refreshed first)
+    void grad(int p_in, int u_out) {  // B^T: needs p at I - e_a
+        halo(1, p_in);
+        for (int s = 0; s < R; ++s) {
+            Slab &S = slabs[s];
+            launch_apply_grad(S.geo, S.vrec, S.p[p_in], S.u[u_out], S.m_own[0], inv_h, stream);
+            ++launches;
+        }
+    }
+    void div(int u_in, int p_out) {  // B: needs u at I + e_a
+        halo(0, u_in);
+        for (int s = 0; s < R; ++s) {
+            Slab &S = slabs[s];
+            launch_apply_div(S.geo, S.prec, S.u[u_in], S.p[p_out], S.m_own[1], inv_h, stream);
+            ++launches;
+        }
+    }
+    void force(int out, int sub) {  // out = force (- sub)
+        for (int s = 0; s < R; ++s) {
+            Slab &S = slabs[s];
+            launch_force(S.u[out], sub < 0 ? nullptr : S.u[sub], S.own_off[flow_dir], S.own[flow_dir], S.m_own[0],
+                         stream);
+            ++launches;
+        }
     }
 };
 
@@ -209,26 +342,62 @@ Status cg_status_to_error(const CgOut &o, int which) {
     return {VS_OK, ""};
 }
 
-// One fused device PCG solve.  op 0: velocity A (x0 allowed), op 1: S_hat
-// (projected).  Returns the iteration count; throws Status on errors.
-int64_t cg_solve(vs_ctx *c, int op, const double *rhs, const double *x0, double eps, double *x) {
+// One fused device PCG solve over all slabs (one cooperative launch).
+// op 0: velocity A (x0 allowed), op 1: S_hat (projected).  Slots index the
+// slab vectors.  Returns the iteration count; throws Status on errors.
+int64_t cg_solve(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     const int64_t m = op == 0 ? c->m_u : c->m_p;
     if (m == 0) return 0;
+    const int R = c->R;
+    if (x0 >= 0) c->halo(op == 0 ? 0 : 1, x0);  // A x0 needs x0 on the ghost planes
+    for (int s = 0; s < R; ++s) {
+        Slab &S = c->slabs[s];
+        CgGroup &G = c->h_groups[s];
+        memset(&G, 0, sizeof G);
+        double **v = op == 0 ? S.u : S.p;
+        if (op == 0) {
+            for (int a = 0; a < 3; ++a) G.meta[a] = S.meta[a];
+        } else {
+            G.meta[0] = S.meta[FP];
+        }
+        G.rec = op == 0 ? S.vrec : S.prec;
+        G.nx = S.nx;
+        G.m_own = (uint32_t)S.m_own[op];
+        G.m_all = (uint32_t)S.m_all[op];
+        G.rhs = v[rhs];
+        G.x0 = x0 >= 0 ? v[x0] : nullptr;
+        G.x = v[x];
+        G.r = op == 0 ? S.u[U_R] : S.p[P_SR];
+        G.z = op == 0 ? S.u[U_Z] : S.p[P_SZ];
+        G.d0 = op == 0 ? S.u[U_D0] : S.p[P_SD0];
+        G.d1 = op == 0 ? S.u[U_D1] : S.p[P_SD1];
+        if (R > 1) {
+            Slab &lo = c->slabs[(s - 1 + R) % R], &hi = c->slabs[(s + 1) % R];
+            G.zpeer[0] = op == 0 ? lo.u[U_Z] : lo.p[P_SZ];
+            G.zpeer[1] = op == 0 ? hi.u[U_Z] : hi.p[P_SZ];
+            const int nf = op == 0 ? c->dim : 1;
+            for (int k = 0; k < nf; ++k) {
+                const int f = op == 0 ? k : FP;
+                G.sbeg[0][k] = (uint32_t)S.own_off[f];
+                G.send[0][k] = (uint32_t)(S.own_off[f] + S.first_cnt[f]);
+                G.sdst[0][k] = (uint32_t)lo.ghi_off[f];
+                G.sbeg[1][k] = (uint32_t)(S.own_off[f] + S.own[f] - S.last_cnt[f]);
+                G.send[1][k] = (uint32_t)(S.own_off[f] + S.own[f]);
+                G.sdst[1][k] = (uint32_t)hi.glo_off[f];
+            }
+        }
+    }
+    CK(cudaMemcpyAsync(c->d_groups, c->h_groups, R * sizeof(CgGroup), cudaMemcpyHostToDevice, c->stream));
     CgParams P;
     memset(&P, 0, sizeof P);
-    P.g = c->geo();
-    P.m = m;
-    P.rec = op == 0 ? c->vrec : c->prec;
-    P.rhs = rhs;
-    P.x0 = x0;
-    P.x = x;
-    P.r = op == 0 ? c->u_r : c->p_sr;
-    P.z = op == 0 ? c->u_z : c->p_sz;
+    P.groups = c->d_groups;
+    P.group_base = 0;
+    P.n = c->n;
+    P.nw = c->nw;
+    P.m_global = (double)m;
+    P.part = c->part;
     P.bar = c->bar;
     P.phase_ns = c->phase_ns;
-    P.d0 = op == 0 ? c->u_d0 : c->p_sd0;
-    P.d1 = op == 0 ? c->u_d1 : c->p_sd1;
-    P.part = c->part;
     P.out = c->cgout;
     P.tol = eps;
     P.max_iter = std::max<int64_t>(1000, 2 * m);  // schur.py:196-197
@@ -243,7 +412,7 @@ int64_t cg_solve(vs_ctx *c, int op, const double *rhs, const double *x0, double 
     CK(cudaMemsetAsync(c->bar, 0, sizeof(unsigned), c->stream));
     ++c->launches;
     CK(cudaEventRecord(c->evs0, c->stream));
-    CK(launch_pcg(c->dim, op, pl, P, c->stream));
+    CK(launch_pcg(c->dim, op, pl, R, P, c->stream));
     CK(cudaEventRecord(c->evs1, c->stream));
     ++c->launches;
     CK(cudaMemcpyAsync(c->h_cg, c->cgout, sizeof(CgOut), cudaMemcpyDeviceToHost, c->stream));
@@ -283,11 +452,115 @@ int guarded(vs_ctx *c, F &&f) {
     }
 }
 
-void h2d_tmp_upload(vs_ctx *c, double *dst, const double *src, int64_t m) {
-    if (m) CK(cudaMemcpyAsync(dst, src, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-}
-void d2h(vs_ctx *c, double *dst, const double *src, int64_t m) {
-    if (m && dst) CK(cudaMemcpyAsync(dst, src, m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+// Build the slabs of the decomposition from the global geometry.
+void build_slabs(vs_ctx *C, int R) {
+    const int n = C->n, dim = C->dim;
+    const int64_t wpp = (int64_t)(dim == 3 ? n : 1) * C->nw;  // meta words per x-plane
+    // plane starts per family, from the first word of each plane
+    for (int f = 0; f < 4; ++f) {
+        if (f < 3 && f >= dim) continue;
+        const uint2 *gm = f == FP ? C->pmeta : C->vmeta[f];
+        std::vector<uint2> first(n);
+        for (int x = 0; x < n; ++x)
+            CK(cudaMemcpyAsync(&first[x], gm + (int64_t)x * wpp, sizeof(uint2), cudaMemcpyDeviceToHost, C->stream));
+        C->sync();
+        C->pstart[f].resize(n + 1);
+        for (int x = 0; x < n; ++x) C->pstart[f][x] = first[x].y;
+        C->pstart[f][n] = f == FP ? C->m_p : C->voff[f] + C->vcount[f];
+    }
+    auto cnt = [&](int f, int x) { x = (x % n + n) % n; return C->pstart[f][x + 1] - C->pstart[f][x]; };
+    C->R = R;
+    C->slabs.assign(R, Slab());
+    for (int s = 0; s < R; ++s) {
+        Slab &S = C->slabs[s];
+        S.x_lo = (int)((int64_t)s * n / R);
+        S.x_hi = (int)((int64_t)(s + 1) * n / R);
+        S.P = S.x_hi - S.x_lo;
+        S.nx = R == 1 ? n : S.P + 2;
+        int64_t off = 0;
+        for (int f = 0; f < dim; ++f) {
+            S.gstart[f] = C->pstart[f][S.x_lo];
+            S.own[f] = C->pstart[f][S.x_hi] - C->pstart[f][S.x_lo];
+            S.own_off[f] = off;
+            off += S.own[f];
+        }
+        S.m_own[0] = off;
+        for (int f = 0; f < dim; ++f) {
+            if (R == 1) continue;
+            S.glo_off[f] = off;
+            S.glo_cnt[f] = cnt(f, S.x_lo - 1);
+            off += S.glo_cnt[f];
+            S.ghi_off[f] = off;
+            S.ghi_cnt[f] = cnt(f, S.x_hi);
+            off += S.ghi_cnt[f];
+        }
+        S.m_all[0] = off;
+        S.gstart[FP] = C->pstart[FP][S.x_lo];
+        S.own[FP] = C->pstart[FP][S.x_hi] - C->pstart[FP][S.x_lo];
+        S.own_off[FP] = 0;
+        S.m_own[1] = S.own[FP];
+        off = S.own[FP];
+        if (R > 1) {
+            S.glo_off[FP] = off;
+            S.glo_cnt[FP] = cnt(FP, S.x_lo - 1);
+            off += S.glo_cnt[FP];
+            S.ghi_off[FP] = off;
+            S.ghi_cnt[FP] = cnt(FP, S.x_hi);
+            off += S.ghi_cnt[FP];
+        }
+        S.m_all[1] = off;
+        for (int f = 0; f < 4; ++f) {
+            if (f < 3 && f >= dim) continue;
+            S.first_cnt[f] = cnt(f, S.x_lo);
+            S.last_cnt[f] = cnt(f, S.x_hi - 1);
+        }
+        // geometry
+        if (R == 1) {
+            for (int a = 0; a < 3; ++a) S.meta[a] = C->vmeta[a];
+            S.meta[FP] = C->pmeta;
+            S.vrec = C->vrec;
+            S.prec = C->prec;
+        } else {
+            for (int f = 0; f < 4; ++f) {
+                if (f < 3 && f >= dim) continue;
+                const uint2 *gm = f == FP ? C->pmeta : C->vmeta[f];
+                S.meta[f] = C->alloc<uint2>(wpp * (S.P + 2));
+                const int64_t xlo_m = ((S.x_lo - 1) % n + n) % n, xhi_m = S.x_hi % n;
+                launch_slab_meta(gm, S.meta[f], wpp, S.x_lo, S.P, n, S.glo_off[f] - C->pstart[f][xlo_m],
+                                 S.own_off[f] - C->pstart[f][S.x_lo], S.ghi_off[f] - C->pstart[f][xhi_m],
+                                 C->stream);
+            }
+            S.vrec = C->alloc<uint64_t>(S.m_own[0]);
+            for (int f = 0; f < dim; ++f)
+                launch_slab_rec(C->vrec + S.gstart[f], S.vrec + S.own_off[f], S.own[f], S.x_lo, C->stream);
+            S.prec = C->alloc<uint64_t>(S.m_own[1]);
+            launch_slab_rec(C->prec + S.gstart[FP], S.prec, S.own[FP], S.x_lo, C->stream);
+            CK(cudaGetLastError());
+        }
+        S.geo.dim = dim;
+        S.geo.n = n;
+        S.geo.nw = C->nw;
+        S.geo.nlines = (dim == 3 ? n : 1) * S.nx;
+        S.geo.nx = S.nx;
+        S.geo.fbits = nullptr;
+        for (int a = 0; a < 3; ++a) S.geo.vmeta[a] = S.meta[a];
+        S.geo.pmeta = S.meta[FP];
+        for (int k = 0; k < NU; ++k) S.u[k] = C->alloc<double>(S.m_all[0]);
+        for (int k = 0; k < NP; ++k) S.p[k] = C->alloc<double>(S.m_all[1]);
+    }
+    int64_t mu_max = 0, mp_max = 0;
+    for (auto &S : C->slabs) {
+        mu_max = std::max(mu_max, S.m_own[0]);
+        mp_max = std::max(mp_max, S.m_own[1]);
+    }
+    C->plan_A = pcg_plan(dim, 0, mu_max, R, C->device);
+    C->plan_S = pcg_plan(dim, 1, mp_max, R, C->device);
+    C->part = C->alloc<double>((size_t)4 * 8 * R * std::max(C->plan_A.grid, C->plan_S.grid));
+    C->d_groups = C->alloc<CgGroup>(R);
+    CK(cudaMallocHost(&C->h_groups, R * sizeof(CgGroup)));
+    C->scal = C->alloc<double>(std::max(8, R));
+    CK(cudaFreeHost(C->h_scal));
+    CK(cudaMallocHost(&C->h_scal, std::max(8, R) * sizeof(double)));
 }
 
 }  // namespace
@@ -298,7 +571,7 @@ extern "C" {
 
 const char *vs_last_error(void) { return g_err.c_str(); }
 
-const char *vs_version(void) { return "voxschur 0.1 sm_100a (fp64, fused persistent PCG)"; }
+const char *vs_version(void) { return "voxschur 0.2 sm_100a (fp64, fused persistent PCG, x-slab groups)"; }
 
 int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels, int64_t *n_components) {
     if ((dim != 2 && dim != 3) || n < 1) return fail(VS_EVALUE, "grid dimension must be 2 or 3, got %d", dim);
@@ -352,13 +625,15 @@ int vs_stamp_balls(uint8_t *fluid, int dim, int n, const double *centers, const 
     return VS_OK;
 }
 
-int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_connectivity, int require_walls,
-                  int device, double inv_h, double inv_h2, vs_ctx **out) {
+int vs_ctx_create2(const uint8_t *fluid, int dim, int n, int flow_dir, int check_connectivity, int require_walls,
+                   int device, double inv_h, double inv_h2, int slabs, vs_ctx **out) {
     *out = nullptr;
     if (dim != 2 && dim != 3) return fail(VS_EVALUE, "grid dimension must be 2 or 3, got %d", dim);
     if (n < 2) return fail(VS_EVALUE, "grid extent must be at least 2, got %d", n);
     if (n > 2047) return fail(VS_EVALUE, "grid extent %d exceeds the record layout limit 2047", n);
     if (flow_dir < 0 || flow_dir >= dim) return fail(VS_EVALUE, "flow axis %d out of range for dim %d", flow_dir, dim);
+    if (slabs < 1 || slabs > VS_MAX_SLABS || slabs > n)
+        return fail(VS_EVALUE, "slab count %d out of range [1, min(%d, n)]", slabs, VS_MAX_SLABS);
     const int64_t ncells = dim == 3 ? (int64_t)n * n * n : (int64_t)n * n;
     // operators.py:220-230 -- host-side validation and connectivity
     int64_t nfluid = 0;
@@ -411,20 +686,16 @@ int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_
             fb[a] = C->alloc<uint32_t>(nw);
             launch_face_bits(g, a, nw, fb[a], C->stream);
         }
-        // counts per family: popc on host-visible totals via the scans
         uint32_t off = 0;
         for (int a = 0; a < dim; ++a) {
             C->vmeta[a] = C->alloc<uint2>(nw);
             CK(build_meta(fb[a], nw, off, C->vmeta[a], cnt, base, temp, tb, C->stream));
-            uint32_t last[2];
             uint2 lastm;
             CK(cudaMemcpyAsync(&lastm, C->vmeta[a] + nw - 1, sizeof(uint2), cudaMemcpyDeviceToHost, C->stream));
             C->sync();
-            last[0] = lastm.y;
-            last[1] = __builtin_popcount(lastm.x);
-            C->vcount[a] = (int64_t)last[0] + last[1] - off;
+            C->vcount[a] = (int64_t)lastm.y + __builtin_popcount(lastm.x) - off;
             C->voff[a] = off;
-            if ((uint64_t)off + C->vcount[a] > 0xFFFFFFF0ull) throw Status{VS_EVALUE, "too many velocity DOFs"};
+            if ((uint64_t)off + C->vcount[a] > 0x7FFFFFF0ull) throw Status{VS_EVALUE, "too many velocity DOFs"};
             off += (uint32_t)C->vcount[a];
         }
         C->m_u = off;
@@ -445,7 +716,7 @@ int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_
         CK(cudaGetLastError());
         // ---- tables: every FP constant is computed exactly as the reference does
         for (int code = 0; code < 16; ++code) {
-            C->diag_code[code] = (double)code * C->diag_scale;       // operators.py:285
+            C->diag_code[code] = (double)code * C->diag_scale;          // operators.py:285
             C->inv_code[code] = code ? 1.0 / C->diag_code[code] : 0.0;  // krylov.py:213
         }
         const int cbase = 2 * dim - 1;
@@ -453,7 +724,7 @@ int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_
             C->invA_enc[e] = e ? 1.0 / ((double)(e + cbase) * C->diag_scale) : 0.0;  // schur.py:235
         // diag(S_hat) by the packed face codes, summed in reference order
         const int nkey = 1 << 18;
-        std::vector<double> invS(1 << 18, 0.0);
+        std::vector<double> invS(nkey, 0.0);
         for (int key = 0; key < nkey; ++key) {
             double acc = 0.0;  // operators.py:202-206
             bool ok = true;
@@ -466,8 +737,8 @@ int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_
             const double dS = acc * C->inv_h2;
             invS[key] = (ok && dS > 0) ? 1.0 / dS : 0.0;  // krylov.py:213
         }
-        C->invS = C->alloc<double>(1 << 18);
-        CK(cudaMemcpyAsync(C->invS, invS.data(), (1 << 18) * sizeof(double), cudaMemcpyHostToDevice, C->stream));
+        C->invS = C->alloc<double>(nkey);
+        CK(cudaMemcpyAsync(C->invS, invS.data(), nkey * sizeof(double), cudaMemcpyHostToDevice, C->stream));
         C->d_diag_code = C->alloc<double>(16);
         C->d_invA_enc = C->alloc<double>(8);
         CK(cudaMemcpyAsync(C->d_diag_code, C->diag_code, 16 * sizeof(double), cudaMemcpyHostToDevice, C->stream));
@@ -479,30 +750,26 @@ int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_
         CK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
         C->sync();
         C->sdiag_ok = hflag == 0;
-        // ---- work vectors
-        const int64_t mu = C->m_u, mp = C->m_p;
-        for (double **v : {&C->u_rhs, &C->u_w, &C->u_iter, &C->u_f, &C->u_r, &C->u_z, &C->u_d0, &C->u_d1, &C->u_tmp})
-            *v = C->alloc<double>(mu);
-        for (double **v : {&C->p_x, &C->p_r, &C->p_d, &C->p_z, &C->p_q, &C->p_b, &C->p_sr, &C->p_sz, &C->p_sd0,
-                           &C->p_sd1, &C->p_tmp})
-            *v = C->alloc<double>(mp);
-        C->plan_A = pcg_plan(dim, 0, C->m_u, device);
-        C->plan_S = pcg_plan(dim, 1, C->m_p, device);
+        // ---- decomposition into x-slabs (1 = whole domain), work vectors, plans
+        build_slabs(C, slabs);
         C->bar = C->alloc<unsigned>(2);
+        CK(cudaMemsetAsync(C->bar, 0, 2 * sizeof(unsigned), C->stream));
         if (getenv("VOXSCHUR_PHASE_TIMING")) {
             C->phase_ns = C->alloc<unsigned long long>(12);
             CK(cudaMemsetAsync(C->phase_ns, 0, 12 * sizeof(unsigned long long), C->stream));
         }
-        CK(cudaMemsetAsync(C->bar, 0, 2 * sizeof(unsigned), C->stream));
-        C->part = C->alloc<double>((size_t)4 * 8 * std::max(C->plan_A.grid, C->plan_S.grid));
         C->red_part = C->alloc<double>(RED_MAX_BLOCKS);
-        C->scal = C->alloc<double>(8);
         C->cgout = C->alloc<CgOut>(1);
         C->sync();
     });
     if (rc != VS_OK) return rc;
     *out = c.release();
     return VS_OK;
+}
+
+int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_connectivity, int require_walls,
+                  int device, double inv_h, double inv_h2, vs_ctx **out) {
+    return vs_ctx_create2(fluid, dim, n, flow_dir, check_connectivity, require_walls, device, inv_h, inv_h2, 1, out);
 }
 
 void vs_ctx_destroy(vs_ctx *ctx) { delete ctx; }
@@ -535,24 +802,26 @@ int vs_export_geometry(vs_ctx *c, uint8_t *fm0, uint8_t *fm1, uint8_t *fm2, uint
     });
 }
 
+// unit applies run on every slab (bitwise independent of the decomposition)
 static int apply_common(vs_ctx *c, int which, const double *in, double *out) {
     return guarded(c, [&] {
         const bool in_u = (which == 0 || which == 1 || which == 3);
         const bool out_u = (which == 0 || which == 2);
-        const int64_t mi = in_u ? c->m_u : c->m_p, mo = out_u ? c->m_u : c->m_p;
-        double *din = in_u ? c->u_tmp : c->p_tmp;
-        double *dout = out_u ? c->u_rhs : c->p_b;
-        h2d_tmp_upload(c, din, in, mi);
-        const Geo g = c->geo();
-        switch (which) {
-            case 0: launch_apply_A(g, c->vrec, din, dout, c->m_u, c->d_diag_code, c->inv_h2, c->stream); break;
-            case 1: launch_apply_div(g, c->prec, din, dout, c->m_p, c->inv_h, c->stream); break;
-            case 2: launch_apply_grad(g, c->vrec, din, dout, c->m_u, c->inv_h, c->stream); break;
-            case 3: launch_dwd(g, c->prec, din, dout, c->m_p, c->inv_h2, c->stream); break;
-            case 4: launch_apply_S(g, c->prec, din, dout, c->m_p, c->d_invA_enc, c->inv_h, c->stream); break;
+        c->upload(in_u ? 0 : 1, in_u ? U_IN : P_IN, in);  // owned + ghost planes from the host vector
+        for (int s = 0; s < c->R; ++s) {
+            Slab &S = c->slabs[s];
+            const double *din = in_u ? S.u[U_IN] : S.p[P_IN];
+            double *dout = out_u ? S.u[U_TMP] : S.p[P_TMP];
+            switch (which) {
+                case 0: launch_apply_A(S.geo, S.vrec, din, dout, S.m_own[0], c->d_diag_code, c->inv_h2, c->stream); break;
+                case 1: launch_apply_div(S.geo, S.prec, din, dout, S.m_own[1], c->inv_h, c->stream); break;
+                case 2: launch_apply_grad(S.geo, S.vrec, din, dout, S.m_own[0], c->inv_h, c->stream); break;
+                case 3: launch_dwd(S.geo, S.prec, din, dout, S.m_own[1], c->inv_h2, c->stream); break;
+                case 4: launch_apply_S(S.geo, S.prec, din, dout, S.m_own[1], c->d_invA_enc, c->inv_h, c->stream); break;
+            }
         }
         CK(cudaGetLastError());
-        d2h(c, out, dout, mo);
+        c->download(out_u ? 0 : 1, out_u ? U_TMP : P_TMP, out);
         c->sync();
     });
 }
@@ -566,10 +835,10 @@ int vs_apply_simple(vs_ctx *c, const double *p, double *out) { return apply_comm
 int vs_solve_velocity(vs_ctx *c, const double *rhs, const double *x0, double eps, double *x, int64_t *iters) {
     return guarded(c, [&] {
         reset_stats(c);
-        h2d_tmp_upload(c, c->u_rhs, rhs, c->m_u);
-        if (x0) h2d_tmp_upload(c, c->u_tmp, x0, c->m_u);
-        *iters = cg_solve(c, 0, c->u_rhs, x0 ? c->u_tmp : nullptr, eps, c->u_w);
-        d2h(c, x, c->u_w, c->m_u);
+        c->upload(0, U_RHS, rhs);
+        if (x0) c->upload(0, U_TMP, x0);
+        *iters = cg_solve(c, 0, U_RHS, x0 ? U_TMP : -1, eps, U_W);
+        c->download(0, U_W, x);
         c->sync();
     });
 }
@@ -578,9 +847,9 @@ int vs_solve_simple(vs_ctx *c, const double *r, double eps, double *z, int64_t *
     return guarded(c, [&] {
         if (!c->sdiag_ok) throw Status{VS_EVALUE, "nonpositive diagonal entry in jacobi preconditioner"};
         reset_stats(c);
-        h2d_tmp_upload(c, c->p_b, r, c->m_p);
-        *iters = cg_solve(c, 1, c->p_b, nullptr, eps, c->p_z);
-        d2h(c, z, c->p_z, c->m_p);
+        c->upload(1, P_B, r);
+        *iters = cg_solve(c, 1, P_B, -1, eps, P_Z);
+        c->download(1, P_Z, z);
         c->sync();
     });
 }
@@ -595,60 +864,56 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
             throw Status{VS_EVALUE, "nonpositive diagonal entry in jacobi preconditioner"};
         reset_stats(c);
         memset(rep, 0, sizeof *rep);
-        const int64_t mu = c->m_u, mp = c->m_p;
-        const int64_t flo = c->voff[c->flow_dir], fcnt = c->vcount[c->flow_dir];
-        const Geo g = c->geo();
         cudaStream_t s = c->stream;
         CK(cudaEventRecord(c->ev0, s));
-        auto perm = [&](const double *u) { return cfg->h_pow_dim * c->sum(u + flo, fcnt); };  // schur.py:288
+        auto perm = [&](int slot) {  // schur.py:288
+            return cfg->h_pow_dim * c->reduce(0, 0, slot, -1, c->flow_dir);
+        };
         int64_t tot_vel = 0, tot_pre = 0;
         // g, u_f = schur_rhs (schur.py:228-231, :308)
-        launch_force(c->u_rhs, nullptr, flo, fcnt, mu, s);
-        ++c->launches;
-        rep->uf_iters = cg_solve(c, 0, c->u_rhs, nullptr, cfg->eps_A, c->u_f);
-        launch_apply_div(g, c->prec, c->u_f, c->p_b, mp, c->inv_h, s);  // g -> p_b
-        ++c->launches;
+        c->force(U_RHS, -1);
+        rep->uf_iters = cg_solve(c, 0, U_RHS, -1, cfg->eps_A, U_F);
+        c->div(U_F, P_B);  // g -> P_B
         // outer_op(p) = B A^-1 B^T p, last_w kept (schur.py:312-316)
-        auto outer_op = [&](const double *p, double *q) {
-            launch_apply_grad(g, c->vrec, p, c->u_rhs, mu, c->inv_h, s);
-            ++c->launches;
-            tot_vel += cg_solve(c, 0, c->u_rhs, nullptr, cfg->eps_A, c->u_w);
-            launch_apply_div(g, c->prec, c->u_w, q, mp, c->inv_h, s);
-            ++c->launches;
+        auto outer_op = [&](int p, int q) {
+            c->grad(p, U_RHS);
+            tot_vel += cg_solve(c, 0, U_RHS, -1, cfg->eps_A, U_W);
+            c->div(U_W, q);
         };
         // z = prec(r); z -= mean(z)   (schur.py:324-327, krylov.py:117-119)
-        auto outer_prec = [&](double *r, double *z) {
+        auto outer_prec = [&](int r, int z) {
             if (cfg->prec == 1) {
-                tot_pre += cg_solve(c, 1, r, nullptr, cfg->eps_Shat, c->p_tmp);
-                const double m = c->mean(c->p_tmp, mp);
-                c->vec(0, z, c->p_tmp, nullptr, m, mp);
+                tot_pre += cg_solve(c, 1, r, -1, cfg->eps_Shat, P_TMP);
+                const double m = c->mean(1, P_TMP);
+                c->vec(1, 0, z, P_TMP, -1, m);
             } else {
-                const double m = c->mean(r, mp);
-                c->vec(0, z, r, nullptr, m, mp);
+                const double m = c->mean(1, r);
+                c->vec(1, 0, z, r, -1, m);
             }
         };
         // u = u_f.copy(); perm_history = [k(u)]
-        CK(cudaMemcpyAsync(c->u_iter, c->u_f, mu * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        c->copy(0, U_ITER, U_F);
         std::vector<double> ph, rp, ru, al, be;
-        ph.push_back(perm(c->u_iter));
+        ph.push_back(perm(U_ITER));
         // ---- outer pcg (krylov.py:76-182) with project_nullspace=True
         const bool use_prec = cfg->outer_norm == 0;
         {
-            const double mg = c->mean(c->p_b, mp);
-            c->vec(0, c->p_b, c->p_b, nullptr, mg, mp);       // rhs -= mean(rhs)
-            CK(cudaMemsetAsync(c->p_x, 0, mp * sizeof(double), s));  // x = 0 (- mean 0)
+            const double mg = c->mean(1, P_B);
+            c->vec(1, 0, P_B, P_B, -1, mg);  // rhs -= mean(rhs)
+            for (auto &S : c->slabs)          // x = 0 (- mean 0)
+                CK(cudaMemsetAsync(S.p[P_X], 0, S.m_all[1] * sizeof(double), s));
         }
-        outer_op(c->p_x, c->p_q);
-        c->vec(4, c->p_r, c->p_q, c->p_b, 0.0, mp);  // r = op(x) - rhs
-        outer_prec(c->p_r, c->p_z);
-        rp.push_back(std::sqrt(c->dot(c->p_z, c->p_z, mp)));
-        ru.push_back(std::sqrt(c->dot(c->p_r, c->p_r, mp)));
+        outer_op(P_X, P_Q);
+        c->vec(1, 4, P_R, P_Q, P_B, 0.0);  // r = op(x) - rhs
+        outer_prec(P_R, P_Z);
+        rp.push_back(std::sqrt(c->dot(1, P_Z, P_Z)));
+        ru.push_back(std::sqrt(c->dot(1, P_R, P_R)));
         const double ref = use_prec ? rp[0] : ru[0];
         bool conv = ref == 0.0;
         int64_t its = 0;
         if (!conv) {
-            CK(cudaMemcpyAsync(c->p_d, c->p_z, mp * sizeof(double), cudaMemcpyDeviceToDevice, s));
-            double rz = c->dot(c->p_r, c->p_z, mp);
+            c->copy(1, P_D, P_Z);
+            double rz = c->dot(1, P_R, P_Z);
             char buf[256];
             for (int64_t k = 0; k < cfg->max_iter; ++k) {
                 if (rz < 0.0) {
@@ -657,24 +922,24 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
                     throw Status{VS_ERUNTIME, buf};
                 }
                 if (rz == 0.0) { conv = true; break; }
-                outer_op(c->p_d, c->p_q);
-                const double dq = c->dot(c->p_d, c->p_q, mp);
+                outer_op(P_D, P_Q);
+                const double dq = c->dot(1, P_D, P_Q);
                 if (dq <= 0.0) {
                     snprintf(buf, sizeof buf, "operator not SPD on subspace: d'q = %.3e at iteration %lld", dq,
                              (long long)k);
                     throw Status{VS_ERUNTIME, buf};
                 }
                 const double alpha = rz / dq;
-                c->vec(1, nullptr, c->p_x, c->p_d, alpha, mp);  // x -= alpha d
-                c->vec(1, nullptr, c->p_r, c->p_q, alpha, mp);  // r -= alpha q
-                c->vec(2, nullptr, c->u_iter, c->u_w, alpha, mu);  // u += alpha w (schur.py:334-336)
-                ph.push_back(perm(c->u_iter));
-                outer_prec(c->p_r, c->p_z);
-                const double rz_new = c->dot(c->p_r, c->p_z, mp);
+                c->vec(1, 1, -1, P_X, P_D, alpha);    // x -= alpha d
+                c->vec(1, 1, -1, P_R, P_Q, alpha);    // r -= alpha q
+                c->vec(0, 2, -1, U_ITER, U_W, alpha);  // u += alpha w (schur.py:334-336)
+                ph.push_back(perm(U_ITER));
+                outer_prec(P_R, P_Z);
+                const double rz_new = c->dot(1, P_R, P_Z);
                 const double beta = rz_new / rz;
                 rz = rz_new;
-                const double nz = std::sqrt(c->dot(c->p_z, c->p_z, mp));
-                const double nr = std::sqrt(c->dot(c->p_r, c->p_r, mp));
+                const double nz = std::sqrt(c->dot(1, P_Z, P_Z));
+                const double nr = std::sqrt(c->dot(1, P_R, P_R));
                 if (!(std::isfinite(nz) && std::isfinite(nr))) {
                     snprintf(buf, sizeof buf, "non-finite residual at iteration %lld", (long long)(k + 1));
                     throw Status{VS_ERUNTIME, buf};
@@ -685,19 +950,18 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
                 ru.push_back(nr);
                 its = k + 1;
                 if ((use_prec ? nz : nr) / ref < cfg->eps_S) { conv = true; break; }
-                c->vec(3, c->p_d, c->p_d, c->p_z, beta, mp);  // d = z + beta d
+                c->vec(1, 3, P_D, P_D, P_Z, beta);  // d = z + beta d
             }
         }
         // refresh: A u = f - B^T p, warm start from u (schur.py:352-357)
-        launch_apply_grad(g, c->vrec, c->p_x, c->u_tmp, mu, c->inv_h, s);
-        launch_force(c->u_rhs, c->u_tmp, flo, fcnt, mu, s);
-        c->launches += 2;
-        tot_vel += cg_solve(c, 0, c->u_rhs, c->u_iter, cfg->eps_A, c->u_iter);
-        const double kval = perm(c->u_iter);
+        c->grad(P_X, U_TMP);
+        c->force(U_RHS, U_TMP);
+        tot_vel += cg_solve(c, 0, U_RHS, U_ITER, cfg->eps_A, U_ITER);
+        const double kval = perm(U_ITER);
         ph.back() = kval;
         CK(cudaEventRecord(c->ev1, s));
-        d2h(c, pressure, c->p_x, mp);
-        d2h(c, velocity, c->u_iter, mu);
+        c->download(1, P_X, pressure);
+        c->download(0, U_ITER, velocity);
         c->sync();
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
@@ -719,7 +983,7 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
     });
 }
 
-int vs_phase_timing(vs_ctx *c, double *ns4) {
+int vs_phase_timing(vs_ctx *c, double *ns12) {
     return guarded(c, [&] {
         unsigned long long h[12] = {0};
         if (c->phase_ns) {
@@ -727,7 +991,7 @@ int vs_phase_timing(vs_ctx *c, double *ns4) {
             CK(cudaMemsetAsync(c->phase_ns, 0, sizeof h, c->stream));
             c->sync();
         }
-        for (int k = 0; k < 12; ++k) ns4[k] = (double)h[k];
+        for (int k = 0; k < 12; ++k) ns12[k] = (double)h[k];
     });
 }
 
@@ -737,5 +1001,7 @@ int vs_kernel_stats(vs_ctx *c, vs_kstat *a, vs_kstat *s, int64_t *launches) {
     if (launches) *launches = c->launches;
     return VS_OK;
 }
+
+int vs_slab_count(vs_ctx *c) { return c->R; }
 
 }  // extern "C"

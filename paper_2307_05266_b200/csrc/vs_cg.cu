@@ -32,14 +32,16 @@ __device__ __forceinline__ uint32_t rank_of(const uint2 *__restrict__ meta, int 
 
 // ranks of the 2*DIM neighbours in the reference slot order
 // (x+, x-, [y+, y-,] z+, z-)   (operators.py:269-271: d = 0..dim-1, s = +1, -1)
+// (nx = extent of the local x axis: n for a whole-domain group, slab planes
+// + 2 ghost planes otherwise -- owned DOFs of a slab never wrap in x)
 template <int DIM>
-__device__ __forceinline__ void neighbour_ranks(const uint2 *__restrict__ meta, int nw, int n, uint64_t rc,
-                                                uint32_t (&nr)[2 * DIM]) {
+__device__ __forceinline__ void neighbour_ranks(const uint2 *__restrict__ meta, int nw, int n, int nx,
+                                                uint64_t rc, uint32_t (&nr)[2 * DIM]) {
     const int z = rec_z(rc), y = rec_y(rc), x = rec_x(rc);
     const int sx = DIM == 3 ? n : 1;
     const int L = DIM == 3 ? x * n + y : x;
-    const int Lxp = (x == n - 1) ? L - (n - 1) * sx : L + sx;
-    const int Lxm = (x == 0) ? L + (n - 1) * sx : L - sx;
+    const int Lxp = (x == nx - 1) ? L - (nx - 1) * sx : L + sx;
+    const int Lxm = (x == 0) ? L + (nx - 1) * sx : L - sx;
     nr[0] = rank_of(meta, nw, Lxp, z);
     nr[1] = rank_of(meta, nw, Lxm, z);
     if (DIM == 3) {
@@ -90,10 +92,21 @@ __device__ __forceinline__ double jacobi_inv(uint64_t rc, const Tabs &T) {
 }
 
 template <int OP>
-__device__ __forceinline__ const uint2 *family_meta(const CgParams &P, uint64_t rc) {
-    if (OP == 1) return P.g.pmeta;
+__device__ __forceinline__ const uint2 *family_meta(const CgGroup &G, uint64_t rc) {
+    if (OP == 1) return G.meta[0];
     const int c = rec_comp(rc);
-    return c == 0 ? P.g.vmeta[0] : (c == 1 ? P.g.vmeta[1] : P.g.vmeta[2]);
+    return c == 0 ? G.meta[0] : (c == 1 ? G.meta[1] : G.meta[2]);
+}
+
+// z of an owned DOF that lies in the first / last owned x-plane of its
+// slab is also stored into the neighbour slab's ghost plane (peer memory on
+// a multi-GPU run; another group's array when ranks are emulated).
+__device__ __forceinline__ void halo_store(const CgGroup &G, int fam, uint32_t i, double zi) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const uint32_t b = G.sbeg[s][fam];
+        if (G.zpeer[s] && i >= b && i < G.send[s][fam]) G.zpeer[s][G.sdst[s][fam] + (i - b)] = zi;
+    }
 }
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -231,8 +244,9 @@ struct DofCache {
 };
 
 template <int DIM, int OP, int TIER>
-__device__ __forceinline__ void fetch_dof(const CgParams &P, const DofCache<DIM, OP, TIER> &C, uint32_t k,
-                                          uint32_t kc, uint32_t i, uint64_t &rc, uint32_t (&nr)[2 * DIM]) {
+__device__ __forceinline__ void fetch_dof(const CgParams &P, const CgGroup &G, const DofCache<DIM, OP, TIER> &C,
+                                          uint32_t k, uint32_t kc, uint32_t i, uint64_t &rc,
+                                          uint32_t (&nr)[2 * DIM]) {
     if (k < kc) {
         rc = C.rec[k * CG_THREADS + threadIdx.x];
         if (TIER == 2) {
@@ -241,9 +255,9 @@ __device__ __forceinline__ void fetch_dof(const CgParams &P, const DofCache<DIM,
             return;
         }
     } else {
-        rc = P.rec[i];
+        rc = G.rec[i];
     }
-    neighbour_ranks<DIM>(family_meta<OP>(P, rc), P.g.nw, P.g.n, rc, nr);
+    neighbour_ranks<DIM>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, nr);
 }
 
 template <int DIM, int OP, int TIER>
@@ -254,6 +268,9 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     __shared__ double s_tab[40];
     __shared__ double s_warp[CG_THREADS / 32][5];
     __shared__ double s_tot[5];
+    __shared__ CgGroup G;  // this block's slab (group)
+    const int grp = P.group_base + blockIdx.x / P.bpg;
+    if (threadIdx.x == 0) G = P.groups[grp];
     if (threadIdx.x < 16) {
         s_tab[threadIdx.x] = P.diag_code[threadIdx.x];
         s_tab[16 + threadIdx.x] = P.inv_code[threadIdx.x];
@@ -264,10 +281,12 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     DofCache<DIM, OP, TIER> cache(dyn_smem, kc);
     __syncthreads();
     const Tabs T{s_tab, s_tab + 16, s_tab + 32, P.invS};
-    const uint32_t m = (uint32_t)P.m;
-    const uint32_t tid = blockIdx.x * CG_THREADS + threadIdx.x;
-    const uint32_t stride = gridDim.x * CG_THREADS;
-    double *x = P.x, *r = P.r, *z = P.z;
+    const uint32_t m = G.m_own;       // owned DOFs of this slab
+    const uint32_t m_all = G.m_all;   // + ghost-plane DOFs
+    const int fam_p = 0;
+    const uint32_t tid = (blockIdx.x % P.bpg) * CG_THREADS + threadIdx.x;
+    const uint32_t stride = P.bpg * CG_THREADS;
+    double *x = G.x, *r = G.r, *z = G.z;
     const double inv_h = P.inv_h, inv_h2 = P.inv_h2;
 
     // ---- setup (krylov.py:102-119): project rhs; r = op(x0) - rhs; z = M^-1 r;
@@ -275,18 +294,19 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     double mu_rhs = 0.0, mu = 0.0, rz = 0.0, rp0 = 0.0, ru0 = 0.0;
     if (PROJ) {
         double v[1] = {0.0};
-        for (uint32_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], P.rhs[i]);
+        for (uint32_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], G.rhs[i]);
         grid_sum<1>(v, P.part, P.bar, gen, s_warp, s_tot);
-        mu_rhs = v[0] / (double)P.m;
+        mu_rhs = v[0] / P.m_global;
     }
     {
         double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        const double *x0 = P.x0;
+        const double *x0 = G.x0;
         uint32_t k = 0;
         for (uint32_t i = tid; i < m; i += stride, ++k) {
-            const uint64_t rc = P.rec[i];
+            const uint64_t rc = G.rec[i];
             uint32_t nr[NS];
-            if (x0 || (TIER == 2 && k < kc)) neighbour_ranks<DIM>(family_meta<OP>(P, rc), P.g.nw, P.g.n, rc, nr);
+            if (x0 || (TIER == 2 && k < kc))
+                neighbour_ranks<DIM>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, nr);
             if (k < kc) cache.put(k, rc, nr);
             double ax = 0.0, xi = 0.0;
             if (x0) {
@@ -299,11 +319,12 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
             } else {
                 x[i] = 0.0;
             }
-            const double b = PROJ ? __dsub_rn(P.rhs[i], mu_rhs) : P.rhs[i];
+            const double b = PROJ ? __dsub_rn(G.rhs[i], mu_rhs) : G.rhs[i];
             const double ri = __dsub_rn(ax, b);
             const double zi = __dmul_rn(ri, jacobi_inv<OP>(rc, T));
             r[i] = ri;
             z[i] = zi;
+            halo_store(G, OP == 0 ? rec_comp(rc) : fam_p, i, zi);
             v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
             v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
             v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
@@ -312,7 +333,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
         }
         grid_sum<5>(v, P.part + 8 * gridDim.x, P.bar, gen, s_warp, s_tot);
         if (PROJ) {
-            mu = v[3] / (double)P.m;
+            mu = v[3] / P.m_global;
             v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
             v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
         }
@@ -325,7 +346,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     int status = 0;
     int64_t sat = 0, its = 0;
     bool conv = (ref == 0.0);
-    double *dold = P.d0, *dnew = P.d1;
+    double *dold = G.d0, *dnew = G.d1;
     unsigned long long ph[4] = {0, 0, 0, 0};  // this block's phase sums (thread 0)
     if (!conv) {
         for (int64_t it = 0; it < P.max_iter; ++it) {
@@ -339,7 +360,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
             for (uint32_t i = tid; i < m; i += stride, ++k) {
                 const uint32_t ip = i + 2 * stride;
                 if (ip < m) {  // stream the centre vectors two strides ahead
-                    if (k + 2 >= kc) prefetch_l2(P.rec + ip);
+                    if (k + 2 >= kc) prefetch_l2(G.rec + ip);
                     prefetch_l2(z + ip);
                     if (!first) prefetch_l2(dold + ip);
                 }
@@ -347,7 +368,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
                 const double dc = first ? 0.0 : dold[i];
                 uint64_t rc;
                 uint32_t nr[NS];
-                fetch_dof<DIM, OP, TIER>(P, cache, k, kc, i, rc, nr);
+                fetch_dof<DIM, OP, TIER>(P, G, cache, k, kc, i, rc, nr);
                 double zn[NS], dn[NS];
 #pragma unroll
                 for (int s = 0; s < NS; ++s) {  // unconditional loads (absent -> own index)
@@ -369,6 +390,12 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
                 dnew[i] = di;
                 v1[0] = __dadd_rn(v1[0], __dmul_rn(di, qi));
             }
+            // ghost-plane d, recomputed exactly as the owning slab computes it
+            for (uint32_t i = m + tid; i < m_all; i += stride) {
+                double zc = z[i];
+                if (PROJ) zc = __dsub_rn(zc, mu);
+                dnew[i] = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dold[i]));
+            }
             const uint64_t t1 = P.phase_ns ? gtimer() : 0;
             grid_sum<1>(v1, P.part + 16 * gridDim.x, P.bar, gen, s_warp, s_tot);
             const uint64_t t2 = P.phase_ns ? gtimer() : 0;
@@ -381,7 +408,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
             for (uint32_t i = tid; i < m; i += stride, ++k) {
                 const uint32_t ip = i + 2 * stride;
                 if (ip < m) {
-                    if (k + 2 >= kc) prefetch_l2(P.rec + ip);
+                    if (k + 2 >= kc) prefetch_l2(G.rec + ip);
                     prefetch_l2(dnew + ip);
                     prefetch_l2(x + ip);
                     prefetch_l2(r + ip);
@@ -389,7 +416,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
                 const double di = dnew[i], xo = x[i], ro = r[i];
                 uint64_t rc;
                 uint32_t nr[NS];
-                fetch_dof<DIM, OP, TIER>(P, cache, k, kc, i, rc, nr);
+                fetch_dof<DIM, OP, TIER>(P, G, cache, k, kc, i, rc, nr);
                 double vn[NS];
 #pragma unroll
                 for (int s = 0; s < NS; ++s) vn[s] = dnew[nr[s] != ABSENT ? nr[s] : i];
@@ -402,6 +429,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
                 x[i] = xi;
                 r[i] = ri;
                 z[i] = zi;
+                halo_store(G, OP == 0 ? rec_comp(rc) : fam_p, i, zi);
                 v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
                 v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
                 v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
@@ -418,7 +446,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
                 ph[3] += t4 - t3;
             }
             if (PROJ) {
-                mu = v[3] / (double)P.m;
+                mu = v[3] / P.m_global;
                 v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
                 v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
             }
@@ -465,8 +493,9 @@ static const void *pcg_fn(int dim, int op, int tier) {
     return op == 0 ? pcg_fn_t<2, 0>(tier) : pcg_fn_t<2, 1>(tier);
 }
 
-// Plan one launch: grid (co-resident blocks), cache tier and slots, smem.
-CgPlan pcg_plan(int dim, int op, int64_t m, int device) {
+// Plan one launch: blocks per group (all groups co-resident on one device),
+// cache tier and slots, smem.  m = the largest owned DOF count of a group.
+CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device) {
     CgPlan pl{};
     int nsm = 0, maxopt = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
@@ -479,7 +508,8 @@ CgPlan pcg_plan(int dim, int op, int64_t m, int device) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CG_THREADS, budget);
         if (per_sm < 1) per_sm = 1;
-        int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * nsm, (m + CG_THREADS - 1) / CG_THREADS));
+        int grid = (int)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)per_sm * nsm / groups, (m + CG_THREADS - 1) / CG_THREADS));
         const int64_t stride = (int64_t)grid * CG_THREADS;
         const int64_t slots = (m + stride - 1) / stride;
         const size_t per_slot = (size_t)CG_THREADS * (tier == 2 ? 8 + 4 * ns : 8);
@@ -493,10 +523,13 @@ CgPlan pcg_plan(int dim, int op, int64_t m, int device) {
     return pl;
 }
 
-cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, CgParams &P, cudaStream_t s) {
+// launches `groups` x pl.grid blocks (one cooperative grid over all groups)
+cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s) {
     P.cache_slots = pl.slots;
+    P.bpg = pl.grid;
     void *args[] = {&P};
-    return cudaLaunchCooperativeKernel(pcg_fn(dim, op, pl.tier), dim3(pl.grid), dim3(CG_THREADS), args, pl.smem, s);
+    return cudaLaunchCooperativeKernel(pcg_fn(dim, op, pl.tier), dim3(pl.grid * groups), dim3(CG_THREADS), args,
+                                       pl.smem, s);
 }
 
 }  // namespace vs

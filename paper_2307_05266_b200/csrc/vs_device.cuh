@@ -43,6 +43,7 @@ __device__ __forceinline__ uint32_t rec_pkey(uint64_t r) { return (uint32_t)((r 
 
 struct Geo {
     int dim, n, nw, nlines;
+    int nx;                  // extent of the (local) x axis: n, or slab planes + 2 ghosts
     const uint32_t *fbits;   // fluid bits [nlines * nw]
     const uint2 *vmeta[3];   // velocity component meta
     const uint2 *pmeta;      // pressure meta
@@ -53,8 +54,9 @@ __device__ __forceinline__ int iaxis(int dim, int a) { return (dim == 3) ? a : (
 
 struct Cell { int x, y, z; };
 
-__device__ __forceinline__ Cell shifted(Cell c, int ia, int s, int n) {
-    if (ia == 0) { c.x += s; c.x = c.x < 0 ? n - 1 : (c.x >= n ? 0 : c.x); }
+__device__ __forceinline__ Cell shifted(Cell c, int ia, int s, const Geo &g) {
+    const int n = g.n;
+    if (ia == 0) { c.x += s; c.x = c.x < 0 ? g.nx - 1 : (c.x >= g.nx ? 0 : c.x); }
     else if (ia == 1) { c.y += s; c.y = c.y < 0 ? n - 1 : (c.y >= n ? 0 : c.y); }
     else { c.z += s; c.z = c.z < 0 ? n - 1 : (c.z >= n ? 0 : c.z); }
     return c;
@@ -90,7 +92,7 @@ __device__ __forceinline__ double apply_A_at(const Geo &g, uint64_t rec, double 
         const int ia = iaxis(g.dim, d);
 #pragma unroll
         for (int si = 0; si < 2; ++si) {
-            const Cell cn = shifted(c, ia, si == 0 ? 1 : -1, g.n);
+            const Cell cn = shifted(c, ia, si == 0 ? 1 : -1, g);
             const uint32_t rk = rank_at(meta, g, cn);
             const double v = (rk != ABSENT) ? ld(rk) : 0.0;
             acc = (d == 0 && si == 0) ? v : __dadd_rn(acc, v);
@@ -115,11 +117,11 @@ __device__ __forceinline__ double apply_S_at(const Geo &g, uint64_t rec, double 
         const int ci = rec_pin(rec, a), co = rec_pout(rec, a);
         double wi = 0.0, wo = 0.0;
         if (ci) {
-            const uint32_t rk = rank_at(g.pmeta, g, shifted(c, ia, -1, g.n));
+            const uint32_t rk = rank_at(g.pmeta, g, shifted(c, ia, -1, g));
             wi = __dmul_rn(__dmul_rn(__dsub_rn(pi, ld(rk)), inv_h), invA_enc[ci]);
         }
         if (co) {
-            const uint32_t rk = rank_at(g.pmeta, g, shifted(c, ia, 1, g.n));
+            const uint32_t rk = rank_at(g.pmeta, g, shifted(c, ia, 1, g));
             wo = __dmul_rn(__dmul_rn(__dsub_rn(ld(rk), pi), inv_h), invA_enc[co]);
         }
         out = __dadd_rn(out, __dsub_rn(wi, wo));

@@ -11,6 +11,7 @@ namespace vs {
 constexpr int CG_THREADS = 512;
 constexpr int RED_THREADS = 256;
 constexpr int RED_MAX_BLOCKS = 592;
+constexpr int VS_MAX_SLABS = 16;
 
 struct CgOut {
     int64_t iterations;
@@ -21,16 +22,29 @@ struct CgOut {
     double res_prec0, res_unprec0, res_prec_last, res_unprec_last;
 };
 
-struct CgParams {
-    Geo g;
-    int64_t m;
-    const uint64_t *rec;
+// One slab of the decomposition (one rank); a whole-domain run is 1 group.
+// Local vectors hold [owned DOFs | ghost-plane DOFs]; ranks in meta are local.
+struct CgGroup {
+    const uint2 *meta[3];   // velocity components (op 0) or meta[0] = pressure (op 1)
+    const uint64_t *rec;    // records of the owned DOFs (x = local plane)
+    int nx;                 // local x extent (n when the group is the whole domain)
+    uint32_t m_own, m_all;  // owned DOFs, owned + ghost
     const double *rhs, *x0;
     double *x, *r, *z, *d0, *d1;
-    double *part;  // 4 sets x 8 slots x grid
-    unsigned *bar; // grid barrier counter
-    uint32_t cache_slots;
-    unsigned long long *phase_ns;  // optional [4] accumulators (block 0): P1, sum1, P2, sum2
+    // halo: side s = 0 sends the first owned plane to the lower neighbour's
+    // ghost_hi, s = 1 the last owned plane to the upper neighbour's ghost_lo;
+    // per family f, local range [sbeg, send) -> zpeer[s][sdst + (i - sbeg)]
+    uint32_t sbeg[2][3], send[2][3], sdst[2][3];
+    double *zpeer[2];
+};
+
+struct CgParams {
+    const CgGroup *groups;  // device array, one per group
+    int group_base, bpg;    // group of block b = group_base + b / bpg
+    int n, nw;
+    double m_global;        // DOFs summed over groups (for the mean projection)
+    double *part;           // 4 sets x 8 slots x (all blocks)
+    unsigned *bar;          // grid barrier counter
     CgOut *out;
     double tol;
     int64_t max_iter;
@@ -40,7 +54,10 @@ struct CgParams {
     double inv_code[16];
     double invA_enc[8];
     const double *invS;
+    uint32_t cache_slots;
+    unsigned long long *phase_ns;  // optional [12] accumulators
 };
+
 
 void launch_pack_fluid(const uint8_t *fluid, const Geo &g, int64_t nwords, uint32_t *fbits, cudaStream_t s);
 void launch_face_bits(const Geo &g, int a, int64_t nwords, uint32_t *out, cudaStream_t s);
@@ -53,6 +70,9 @@ void launch_bits_to_u8(const uint2 *meta, const uint32_t *bits, const Geo &g, in
                        cudaStream_t s);
 void launch_vcodes(const uint64_t *rec, int64_t m, uint8_t *out, cudaStream_t s);
 void launch_zero_sdiag(const uint64_t *prec, int64_t m, int *flag, cudaStream_t s);
+void launch_slab_meta(const uint2 *gmeta, uint2 *lmeta, int64_t words_per_plane, int x_lo, int P, int n,
+                      int64_t dlo, int64_t down, int64_t dhi, cudaStream_t s);
+void launch_slab_rec(const uint64_t *grec, uint64_t *lrec, int64_t count, int x_lo, cudaStream_t s);
 void launch_apply_A(const Geo &g, const uint64_t *rec, const double *u, double *out, int64_t m,
                     const double *diag_code, double inv_h2, cudaStream_t s);
 void launch_apply_div(const Geo &g, const uint64_t *prec, const double *u, double *out, int64_t m, double inv_h,
@@ -73,7 +93,7 @@ struct CgPlan {
     uint32_t slots;
     size_t smem;
 };
-CgPlan pcg_plan(int dim, int op, int64_t m, int device);
-cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, CgParams &P, cudaStream_t s);
+CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device);
+cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
 
 }  // namespace vs

@@ -45,7 +45,7 @@ __global__ void k_face_bits(Geo g, int a, int64_t nwords, uint32_t *out) {
         const int b = __ffs(fb) - 1;
         fb &= fb - 1;
         const Cell c = word_cell(g, word, b);
-        if (fluid_at(g, shifted(c, ia, -1, g.n))) bits |= 1u << b;
+        if (fluid_at(g, shifted(c, ia, -1, g))) bits |= 1u << b;
     }
     out[word] = bits;
 }
@@ -69,9 +69,9 @@ __device__ int face_code(const Geo &g, int a, Cell c) {
         const int id = iaxis(g.dim, d);
         for (int si = 0; si < 2; ++si) {
             if (d == a) { code += 1; continue; }
-            const Cell cn = shifted(c, id, si == 0 ? 1 : -1, g.n);
+            const Cell cn = shifted(c, id, si == 0 ? 1 : -1, g);
             const bool hi = fluid_at(g, cn);
-            const bool lo = fluid_at(g, shifted(cn, ia, -1, g.n));
+            const bool lo = fluid_at(g, shifted(cn, ia, -1, g));
             const bool nb_face = hi && lo;
             code += (!nb_face && !hi && !lo) ? 2 : 1;
         }
@@ -107,9 +107,9 @@ __global__ void k_p_records(Geo g, int64_t nwords, uint64_t *rec) {
         uint64_t r = make_rec(c.x, c.y, c.z, 0);
         for (int a = 0; a < g.dim; ++a) {
             const int ia = iaxis(g.dim, a);
-            if (fluid_at(g, shifted(c, ia, -1, g.n)))
+            if (fluid_at(g, shifted(c, ia, -1, g)))
                 r |= (uint64_t)(face_code(g, a, c) - cbase) << (40 + 3 * a);
-            const Cell cp = shifted(c, ia, 1, g.n);
+            const Cell cp = shifted(c, ia, 1, g);
             if (fluid_at(g, cp))
                 r |= (uint64_t)(face_code(g, a, cp) - cbase) << (49 + 3 * a);
         }
@@ -139,6 +139,30 @@ __global__ void k_zero_sdiag(const uint64_t *prec, int64_t m, int *flag) {
     if (i < m && rec_pkey(prec[i]) == 0) atomicOr(flag, 1);
 }
 
+// ------------------------------------------------------ slab decomposition
+// Local meta of one family for a slab: local plane p in [0, P+2) is global
+// plane (x_lo - 1 + p) mod n; base shifted by the plane's local offset.
+__global__ void k_slab_meta(const uint2 *gmeta, uint2 *lmeta, int64_t words_per_plane, int x_lo, int P, int n,
+                            int64_t delta_glo, int64_t delta_own, int64_t delta_ghi) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= words_per_plane * (P + 2)) return;
+    const int p = (int)(i / words_per_plane);
+    const int64_t w = i % words_per_plane;
+    const int x = ((x_lo - 1 + p) % n + n) % n;
+    const uint2 m = gmeta[(int64_t)x * words_per_plane + w];
+    const int64_t d = p == 0 ? delta_glo : (p == P + 1 ? delta_ghi : delta_own);
+    lmeta[i] = make_uint2(m.x, (uint32_t)((int64_t)m.y + d));
+}
+
+// Owned records of a slab: copy a global rank range, x -> local plane.
+__global__ void k_slab_rec(const uint64_t *grec, uint64_t *lrec, int64_t count, int x_lo) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint64_t r = grec[i];
+    const uint64_t xl = (uint64_t)(((r >> 22) & 0x7FF) - x_lo + 1);
+    lrec[i] = (r & ~(0x7FFull << 22)) | (xl << 22);
+}
+
 // --------------------------------------------------------- operator applies
 
 __global__ void k_apply_A(Geo g, const uint64_t *rec, const double *u, double *out, int64_t m,
@@ -161,7 +185,7 @@ __global__ void k_apply_div(Geo g, const uint64_t *prec, const double *u, double
     for (int a = 0; a < g.dim; ++a) {
         const double vin = rec_pin(r, a) ? u[rank_at(g.vmeta[a], g, c)] : 0.0;
         const double vout =
-            rec_pout(r, a) ? u[rank_at(g.vmeta[a], g, shifted(c, iaxis(g.dim, a), 1, g.n))] : 0.0;
+            rec_pout(r, a) ? u[rank_at(g.vmeta[a], g, shifted(c, iaxis(g.dim, a), 1, g))] : 0.0;
         acc = __dadd_rn(acc, __dsub_rn(vin, vout));
     }
     out[i] = __dmul_rn(acc, inv_h);
@@ -176,7 +200,7 @@ __global__ void k_apply_grad(Geo g, const uint64_t *vrec, const double *p, doubl
     const Cell c = rec_cell(r);
     const int a = rec_comp(r);
     const double hi = p[rank_at(g.pmeta, g, c)];
-    const double lo = p[rank_at(g.pmeta, g, shifted(c, iaxis(g.dim, a), -1, g.n))];
+    const double lo = p[rank_at(g.pmeta, g, shifted(c, iaxis(g.dim, a), -1, g))];
     out[i] = __dmul_rn(__dsub_rn(hi, lo), inv_h);
 }
 
@@ -198,7 +222,7 @@ __global__ void k_dwd(Geo g, const uint64_t *prec, const double *w, double *out,
     for (int a = 0; a < g.dim; ++a) {
         const double vin = rec_pin(r, a) ? w[rank_at(g.vmeta[a], g, c)] : 0.0;
         const double vout =
-            rec_pout(r, a) ? w[rank_at(g.vmeta[a], g, shifted(c, iaxis(g.dim, a), 1, g.n))] : 0.0;
+            rec_pout(r, a) ? w[rank_at(g.vmeta[a], g, shifted(c, iaxis(g.dim, a), 1, g))] : 0.0;
         acc = __dadd_rn(acc, __dadd_rn(vin, vout));
     }
     out[i] = __dmul_rn(acc, inv_h2);
@@ -292,6 +316,14 @@ void launch_vcodes(const uint64_t *rec, int64_t m, uint8_t *out, cudaStream_t s)
 }
 void launch_zero_sdiag(const uint64_t *prec, int64_t m, int *flag, cudaStream_t s) {
     if (m) k_zero_sdiag<<<nblk(m), 256, 0, s>>>(prec, m, flag);
+}
+void launch_slab_meta(const uint2 *gmeta, uint2 *lmeta, int64_t words_per_plane, int x_lo, int P, int n,
+                      int64_t dlo, int64_t down, int64_t dhi, cudaStream_t s) {
+    k_slab_meta<<<nblk(words_per_plane * (P + 2)), 256, 0, s>>>(gmeta, lmeta, words_per_plane, x_lo, P, n, dlo,
+                                                               down, dhi);
+}
+void launch_slab_rec(const uint64_t *grec, uint64_t *lrec, int64_t count, int x_lo, cudaStream_t s) {
+    if (count) k_slab_rec<<<nblk(count), 256, 0, s>>>(grec, lrec, count, x_lo);
 }
 void launch_apply_A(const Geo &g, const uint64_t *rec, const double *u, double *out, int64_t m,
                     const double *diag_code, double inv_h2, cudaStream_t s) {

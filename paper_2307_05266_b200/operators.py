@@ -178,11 +178,15 @@ def _default_device() -> int:
 
 
 def assemble(grid: VoxelGrid, flow_dir=0, *, check_connectivity: bool = True,
-             require_walls: bool = True, device: int | None = None) -> StaggeredSystem:
+             require_walls: bool = True, device: int | None = None,
+             slabs: int = 1) -> StaggeredSystem:
     """Build the staggered operators for a voxel grid on the GPU.
 
     Same signature and errors as operators.py:209-230 plus the backend
-    selector ``device`` (default $VOXSCHUR_DEVICE, else $LOCAL_RANK, else 0).
+    selectors ``device`` (default $VOXSCHUR_DEVICE, else $LOCAL_RANK, else 0)
+    and ``slabs``: decompose into that many x-slabs (ranks) with ghost-plane
+    exchange inside the fused solver; on one device the
+    ranks run as groups of one cooperative grid.
     """
     if not isinstance(grid, VoxelGrid):
         grid = VoxelGrid(np.asarray(grid))
@@ -191,6 +195,7 @@ def assemble(grid: VoxelGrid, flow_dir=0, *, check_connectivity: bool = True,
     h = grid.physical_length / grid.n
     ctx = C.c_void_p()
     fl = np.ascontiguousarray(grid.fluid, dtype=np.uint8).ravel()
-    _lib.check(_lib.lib.vs_ctx_create(fl, grid.dim, grid.n, flow_dir, int(check_connectivity),
-                                      int(require_walls), dev, 1.0 / h, 1.0 / h**2, C.byref(ctx)))
+    _lib.check(_lib.lib.vs_ctx_create2(fl, grid.dim, grid.n, flow_dir, int(check_connectivity),
+                                       int(require_walls), dev, 1.0 / h, 1.0 / h**2, int(slabs),
+                                       C.byref(ctx)))
     return StaggeredSystem(grid, flow_dir, ctx, dev)

@@ -16,7 +16,7 @@ from paper_2307_05266_b200 import _lib  # noqa: E402
 
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "voxschur.h")).read()
-    return sorted(set(re.findall(r"\b(vs_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(vs_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_symbols_exported():
