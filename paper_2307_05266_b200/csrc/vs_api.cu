@@ -112,6 +112,7 @@ struct vs_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
     vs_kstat st_A{}, st_S{};  // stats of the last top-level call
     int64_t launches = 0;
+    uint32_t pf_dist = 2;  // VOXSCHUR_PREFETCH overrides
 
     Geo geo() const {
         Geo g;
@@ -408,6 +409,7 @@ int64_t cg_solve(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     memcpy(P.inv_code, c->inv_code, sizeof P.inv_code);
     memcpy(P.invA_enc, c->invA_enc, sizeof P.invA_enc);
     P.invS = c->invS;
+    P.pf_dist = c->pf_dist;
     const CgPlan &pl = op == 0 ? c->plan_A : c->plan_S;
     CK(cudaMemsetAsync(c->bar, 0, sizeof(unsigned), c->stream));
     ++c->launches;
@@ -754,6 +756,7 @@ int vs_ctx_create2(const uint8_t *fluid, int dim, int n, int flow_dir, int check
         build_slabs(C, slabs);
         C->bar = C->alloc<unsigned>(2);
         CK(cudaMemsetAsync(C->bar, 0, 2 * sizeof(unsigned), C->stream));
+        if (const char *pf = getenv("VOXSCHUR_PREFETCH")) C->pf_dist = (uint32_t)atoi(pf);
         if (getenv("VOXSCHUR_PHASE_TIMING")) {
             C->phase_ns = C->alloc<unsigned long long>(12);
             CK(cudaMemsetAsync(C->phase_ns, 0, 12 * sizeof(unsigned long long), C->stream));

@@ -358,8 +358,8 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
             double v1[1] = {0.0};
             uint32_t k = 0;
             for (uint32_t i = tid; i < m; i += stride, ++k) {
-                const uint32_t ip = i + 2 * stride;
-                if (ip < m) {  // stream the centre vectors two strides ahead
+                const uint32_t ip = i + P.pf_dist * stride;
+                if (P.pf_dist && ip < m) {  // stream the centre vectors pf_dist strides ahead
                     if (k + 2 >= kc) prefetch_l2(G.rec + ip);
                     prefetch_l2(z + ip);
                     if (!first) prefetch_l2(dold + ip);
@@ -406,8 +406,8 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
             double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
             k = 0;
             for (uint32_t i = tid; i < m; i += stride, ++k) {
-                const uint32_t ip = i + 2 * stride;
-                if (ip < m) {
+                const uint32_t ip = i + P.pf_dist * stride;
+                if (P.pf_dist && ip < m) {
                     if (k + 2 >= kc) prefetch_l2(G.rec + ip);
                     prefetch_l2(dnew + ip);
                     prefetch_l2(x + ip);

@@ -55,6 +55,7 @@ struct CgParams {
     double invA_enc[8];
     const double *invS;
     uint32_t cache_slots;
+    uint32_t pf_dist;              // L2 prefetch distance in grid strides (0 = off)
     unsigned long long *phase_ns;  // optional [12] accumulators
 };
 
