@@ -99,6 +99,12 @@ int vs_ctx_create2(const uint8_t *fluid, int dim, int n, int flow_dir,
                    double inv_h, double inv_h2, int slabs, vs_ctx **out);
 int vs_slab_count(vs_ctx *ctx);
 
+/* Host-only slab plan of a mask (no device needed): for each slab 42 int64 =
+ * x_lo, x_hi; per family (velocity 0, 1, 2, pressure): own, own_off,
+ * glo_off, glo_cnt, ghi_off, ghi_cnt, first_cnt, last_cnt, gstart; then
+ * m_own[vel, p], m_all[vel, p].  Local vectors are [owned | ghost planes]. */
+int vs_slab_plan(const uint8_t *fluid, int dim, int n, int slabs, int64_t *out);
+
 /* DofMap sizes (operators.py:233-235, :247). */
 int vs_counts(vs_ctx *ctx, int64_t *m_u, int64_t *m_p, int64_t axis_counts[3]);
 

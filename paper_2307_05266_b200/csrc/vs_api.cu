@@ -454,35 +454,21 @@ int guarded(vs_ctx *c, F &&f) {
     }
 }
 
-// Build the slabs of the decomposition from the global geometry.
-void build_slabs(vs_ctx *C, int R) {
-    const int n = C->n, dim = C->dim;
-    const int64_t wpp = (int64_t)(dim == 3 ? n : 1) * C->nw;  // meta words per x-plane
-    // plane starts per family, from the first word of each plane
-    for (int f = 0; f < 4; ++f) {
-        if (f < 3 && f >= dim) continue;
-        const uint2 *gm = f == FP ? C->pmeta : C->vmeta[f];
-        std::vector<uint2> first(n);
-        for (int x = 0; x < n; ++x)
-            CK(cudaMemcpyAsync(&first[x], gm + (int64_t)x * wpp, sizeof(uint2), cudaMemcpyDeviceToHost, C->stream));
-        C->sync();
-        C->pstart[f].resize(n + 1);
-        for (int x = 0; x < n; ++x) C->pstart[f][x] = first[x].y;
-        C->pstart[f][n] = f == FP ? C->m_p : C->voff[f] + C->vcount[f];
-    }
-    auto cnt = [&](int f, int x) { x = (x % n + n) % n; return C->pstart[f][x + 1] - C->pstart[f][x]; };
-    C->R = R;
-    C->slabs.assign(R, Slab());
+// Layout of every slab from the per-family plane starts (host only; shared
+// by the device build and the vs_slab_plan ABI used by the CPU tests).
+void plan_slabs(const std::vector<int64_t> (&pstart)[4], int n, int dim, int R, std::vector<Slab> &slabs) {
+    auto cnt = [&](int f, int x) { x = (x % n + n) % n; return pstart[f][x + 1] - pstart[f][x]; };
+    slabs.assign(R, Slab());
     for (int s = 0; s < R; ++s) {
-        Slab &S = C->slabs[s];
+        Slab &S = slabs[s];
         S.x_lo = (int)((int64_t)s * n / R);
         S.x_hi = (int)((int64_t)(s + 1) * n / R);
         S.P = S.x_hi - S.x_lo;
         S.nx = R == 1 ? n : S.P + 2;
         int64_t off = 0;
         for (int f = 0; f < dim; ++f) {
-            S.gstart[f] = C->pstart[f][S.x_lo];
-            S.own[f] = C->pstart[f][S.x_hi] - C->pstart[f][S.x_lo];
+            S.gstart[f] = pstart[f][S.x_lo];
+            S.own[f] = pstart[f][S.x_hi] - pstart[f][S.x_lo];
             S.own_off[f] = off;
             off += S.own[f];
         }
@@ -497,8 +483,8 @@ void build_slabs(vs_ctx *C, int R) {
             off += S.ghi_cnt[f];
         }
         S.m_all[0] = off;
-        S.gstart[FP] = C->pstart[FP][S.x_lo];
-        S.own[FP] = C->pstart[FP][S.x_hi] - C->pstart[FP][S.x_lo];
+        S.gstart[FP] = pstart[FP][S.x_lo];
+        S.own[FP] = pstart[FP][S.x_hi] - pstart[FP][S.x_lo];
         S.own_off[FP] = 0;
         S.m_own[1] = S.own[FP];
         off = S.own[FP];
@@ -516,6 +502,29 @@ void build_slabs(vs_ctx *C, int R) {
             S.first_cnt[f] = cnt(f, S.x_lo);
             S.last_cnt[f] = cnt(f, S.x_hi - 1);
         }
+    }
+}
+
+// Build the slabs of the decomposition from the global geometry.
+void build_slabs(vs_ctx *C, int R) {
+    const int n = C->n, dim = C->dim;
+    const int64_t wpp = (int64_t)(dim == 3 ? n : 1) * C->nw;  // meta words per x-plane
+    // plane starts per family, from the first word of each plane
+    for (int f = 0; f < 4; ++f) {
+        if (f < 3 && f >= dim) continue;
+        const uint2 *gm = f == FP ? C->pmeta : C->vmeta[f];
+        std::vector<uint2> first(n);
+        for (int x = 0; x < n; ++x)
+            CK(cudaMemcpyAsync(&first[x], gm + (int64_t)x * wpp, sizeof(uint2), cudaMemcpyDeviceToHost, C->stream));
+        C->sync();
+        C->pstart[f].resize(n + 1);
+        for (int x = 0; x < n; ++x) C->pstart[f][x] = first[x].y;
+        C->pstart[f][n] = f == FP ? C->m_p : C->voff[f] + C->vcount[f];
+    }
+    C->R = R;
+    plan_slabs(C->pstart, n, dim, R, C->slabs);
+    for (int s = 0; s < R; ++s) {
+        Slab &S = C->slabs[s];
         // geometry
         if (R == 1) {
             for (int a = 0; a < 3; ++a) S.meta[a] = C->vmeta[a];
@@ -624,6 +633,55 @@ int vs_stamp_balls(uint8_t *fluid, int dim, int n, const double *centers, const 
     }
     *used = k;
     *n_fluid = nf;
+    return VS_OK;
+}
+
+// Host-only slab plan of a mask (no device): per slab 42 int64 =
+// x_lo, x_hi, then per family f in (0,1,2,pressure): own, own_off, glo_off,
+// glo_cnt, ghi_off, ghi_cnt, first_cnt, last_cnt, gstart; then m_own[2], m_all[2].
+int vs_slab_plan(const uint8_t *fluid, int dim, int n, int slabs, int64_t *out) {
+    if ((dim != 2 && dim != 3) || n < 2) return fail(VS_EVALUE, "bad grid for vs_slab_plan");
+    if (slabs < 1 || slabs > VS_MAX_SLABS || slabs > n)
+        return fail(VS_EVALUE, "slab count %d out of range [1, min(%d, n)]", slabs, VS_MAX_SLABS);
+    const int64_t plane = dim == 3 ? (int64_t)n * n : n;
+    const int64_t st[3] = {plane, dim == 3 ? (int64_t)n : 1, 1};
+    std::vector<int64_t> ps[4];
+    std::vector<int64_t> c(n);
+    int64_t off = 0;
+    for (int f = 0; f < 4; ++f) {
+        if (f < 3 && f >= dim) continue;
+        std::fill(c.begin(), c.end(), 0);
+        for (int x = 0; x < n; ++x)
+            for (int64_t q = 0; q < plane; ++q) {
+                const int64_t i = (int64_t)x * plane + q;
+                if (!fluid[i]) continue;
+                if (f == FP) { ++c[x]; continue; }
+                // face (f, I): fluid[I] && fluid[I - e_f] (operators.py:232)
+                const int64_t coord = (i / st[f]) % n;
+                const int64_t j = coord == 0 ? i + (int64_t)(n - 1) * st[f] : i - st[f];
+                if (fluid[j]) ++c[x];
+            }
+        ps[f].assign(n + 1, 0);
+        int64_t acc = f == FP ? 0 : off;
+        for (int x = 0; x < n; ++x) { ps[f][x] = acc; acc += c[x]; }
+        ps[f][n] = acc;
+        if (f != FP) off = acc;
+    }
+    std::vector<Slab> sl;
+    plan_slabs(ps, n, dim, slabs, sl);
+    for (int s = 0; s < slabs; ++s) {
+        const Slab &S = sl[s];
+        int64_t *o = out + (int64_t)s * 42;
+        o[0] = S.x_lo;
+        o[1] = S.x_hi;
+        for (int f = 0; f < 4; ++f) {
+            int64_t *q = o + 2 + 9 * f;
+            q[0] = S.own[f]; q[1] = S.own_off[f]; q[2] = S.glo_off[f]; q[3] = S.glo_cnt[f];
+            q[4] = S.ghi_off[f]; q[5] = S.ghi_cnt[f]; q[6] = S.first_cnt[f]; q[7] = S.last_cnt[f];
+            q[8] = S.gstart[f];
+        }
+        o[38] = S.m_own[0]; o[39] = S.m_own[1]; o[40] = S.m_all[0]; o[41] = S.m_all[1];
+    }
     return VS_OK;
 }
 
