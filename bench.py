@@ -25,11 +25,18 @@ device time ("scaling": "weak").
 """
 from __future__ import annotations
 
+import os
+
+# the CPU legs are single-threaded numpy by design (multi-threaded
+# OpenBLAS under contention is ~28x slower); pin before numpy is imported, so
+# spawned worker processes inherit it too
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
 import argparse
 import json
 import math
 import multiprocessing as mp
-import os
 import statistics
 import subprocess
 import sys
@@ -157,17 +164,18 @@ def run_reference(a):
     if rank != 0:
         return 0
     cores = usable_cores()
-    vals = []
+    vals, secs = [], []
     for i in range(a.warmup + a.steps):
         v, res = cpu_sample(a.config, a.seed, cores)
         if i >= a.warmup:
             vals.append(v)
+            secs.append(max(r["seconds"] for r in res))
     val = statistics.median(vals)
     spec = __import__("paper_2307_05266_b200.configs", fromlist=["CONFIGS"]).CONFIGS[a.config]
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "Gcell/s",
         "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": spec.name, "seed": a.seed, "precs": list(spec.precs)},
         "cpu_baseline": {"value": val, "unit": "Gcell/s", "cores": cores, "kind": "port",
@@ -282,7 +290,6 @@ def run_ours(a):
     # dominant kernel: the fused persistent PCG with the larger share
     domS = tot["msS"] >= tot["msA"]
     dof_k, ms_k, l_k = (tot["dofS"], tot["msS"], tot["lS"]) if domS else (tot["dofA"], tot["msA"], tot["lA"])
-    peak, peak_kind = measured_peak()
     achieved = BYTES_PER_DOF_ITER * dof_k / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -297,6 +304,35 @@ def run_ours(a):
                 "bytes_per_launch": BYTES_PER_DOF_ITER * dof_k / max(1, l_k),
                 "peak_kind": peak_kind, "frac_vs_8TBs": achieved / 8000.0,
                 "share_of_step": (ms_k / tot["ms"]) if tot["ms"] else None}
+
+    peak, peak_kind = measured_peak()
+    # HBM regime: the same fused kernels on C2 (256^3, working set > L2), one
+    # inner A-solve and one inner S_hat-solve (SURVEY 8d per-iteration roofline)
+    hbm = None
+    if not a.no_hbm:
+        g2 = configs.make_geometry("C2", a.seed)
+        s2 = vx.assemble(g2, 0, device=dev)
+        rng = np.random.default_rng(1)
+        pz = rng.standard_normal(s2.m_p)
+        pz -= pz.mean()
+        rhs = s2.apply_gradient(pz)
+        for _ in range(2):  # first = warm-up
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            vx.schur._solve_velocity(s2, rhs, 1e-12)
+            stA = vx.last_kernel_stats(s2)["velocity_cg"]
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            vx.apply_simple_inverse(s2, pz, 1e-12)
+            stS = vx.last_kernel_stats(s2)["simple_cg"]
+        def rl(st):
+            ach = BYTES_PER_DOF_ITER * st["dof_iters"] / (st["ms"] / 1e3) / 1e9
+            return {"iterations": st["iterations"], "us_per_iteration": 1e3 * st["ms"] / st["iterations"],
+                    "achieved": ach, "frac": ach / peak}
+        hbm = {"workload": "C2 256^3 spheres phi0.15 (m_u %d, m_p %d): one inner A-solve and one inner "
+                           "S_hat-solve to 1e-12" % (s2.m_u, s2.m_p),
+               "unit": "GB/s", "peak": peak, "k_pcg_A": rl(stA), "k_pcg_S": rl(stS)}
+        del s2
 
     line = None
     if rank == 0:
@@ -323,7 +359,7 @@ def run_ours(a):
             "time_to_tol_ms": {r["prec"]: r["device_ms"] for r in last},
             "solves": last,
             "inner_iterations_per_step": {"A": tot["IA"] // a.steps, "S_hat": tot["IS"] // a.steps},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "roofline_hbm_regime": hbm, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": tot["launches"], "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -342,6 +378,7 @@ def main():
     ap.add_argument("--config", default="C1")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-hbm", action="store_true", help="skip the C2 HBM-regime kernel measurement")
     a = ap.parse_args()
     if a.warmup < 3:
         print("warning: the timing rules require --warmup >= 3", file=sys.stderr)
