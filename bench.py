@@ -287,6 +287,7 @@ def run_ours(a):
            "includes": "assemble (host connectivity check + H2D mask + device geometry build) "
                        "+ solves + D2H p,u,histories"}
 
+    peak, peak_kind = measured_peak()
     # dominant kernel: the fused persistent PCG with the larger share
     domS = tot["msS"] >= tot["msA"]
     dof_k, ms_k, l_k = (tot["dofS"], tot["msS"], tot["lS"]) if domS else (tot["dofA"], tot["msA"], tot["lA"])
@@ -305,7 +306,6 @@ def run_ours(a):
                 "peak_kind": peak_kind, "frac_vs_8TBs": achieved / 8000.0,
                 "share_of_step": (ms_k / tot["ms"]) if tot["ms"] else None}
 
-    peak, peak_kind = measured_peak()
     # HBM regime: the same fused kernels on C2 (256^3, working set > L2), one
     # inner A-solve and one inner S_hat-solve (SURVEY 8d per-iteration roofline)
     hbm = None
