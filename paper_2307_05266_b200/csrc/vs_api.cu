@@ -112,7 +112,7 @@ struct vs_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
     vs_kstat st_A{}, st_S{};  // stats of the last top-level call
     int64_t launches = 0;
-    uint32_t pf_dist = 2;  // VOXSCHUR_PREFETCH overrides
+    uint32_t pf_dist = 0;  // L2 prefetch (measured neutral); VOXSCHUR_PREFETCH overrides
 
     Geo geo() const {
         Geo g;

@@ -93,9 +93,15 @@ __device__ __forceinline__ double jacobi_inv(uint64_t rc, const Tabs &T) {
 
 template <int OP>
 __device__ __forceinline__ const uint2 *family_meta(const CgGroup &G, uint64_t rc) {
-    if (OP == 1) return G.meta[0];
-    const int c = rec_comp(rc);
-    return c == 0 ? G.meta[0] : (c == 1 ? G.meta[1] : G.meta[2]);
+    const uint2 *m;
+    if (OP == 1) {
+        m = G.meta[0];
+    } else {
+        const int c = rec_comp(rc);
+        m = c == 0 ? G.meta[0] : (c == 1 ? G.meta[1] : G.meta[2]);
+    }
+    __builtin_assume(__isGlobal(m));
+    return m;
 }
 
 // z of an owned DOF that lies in the first / last owned x-plane of its
@@ -105,7 +111,11 @@ __device__ __forceinline__ void halo_store(const CgGroup &G, int fam, uint32_t i
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
         const uint32_t b = G.sbeg[s][fam];
-        if (G.zpeer[s] && i >= b && i < G.send[s][fam]) G.zpeer[s][G.sdst[s][fam] + (i - b)] = zi;
+        if (i >= b && i < G.send[s][fam]) {
+            double *dst = G.zpeer[s];
+            __builtin_assume(__isGlobal(dst));
+            dst[G.sdst[s][fam] + (i - b)] = zi;
+        }
     }
 }
 
@@ -125,6 +135,11 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -134,13 +149,17 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
 // one red.release per block, then thread 0 polls with acquire loads.
 // (Measured on B200: ~1.2-1.4 us per barrier for 148-296 blocks, the same
 // as cooperative_groups grid.sync; tools/gridsync_micro.cu.)
+// Polling uses relaxed loads: an acquire load per poll makes ptxas emit an
+// L1 invalidation (CCTL.IVALL) per poll, which wipes the L1 of the other
+// block still computing on the same SM.  One acquire fence after the poll.
 __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target) {
     __syncthreads();
     target += gridDim.x;
     if (threadIdx.x == 0) {
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-        while ((int)(ld_acquire(bar) - target) < 0) {
+        while ((int)(ld_relaxed(bar) - target) < 0) {
         }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
 }
@@ -255,7 +274,9 @@ __device__ __forceinline__ void fetch_dof(const CgParams &P, const CgGroup &G, c
             return;
         }
     } else {
-        rc = G.rec[i];
+        const uint64_t *rec = G.rec;
+        __builtin_assume(__isGlobal(rec));
+        rc = rec[i];
     }
     neighbour_ranks<DIM>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, nr);
 }
@@ -287,6 +308,12 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     const uint32_t tid = (blockIdx.x % P.bpg) * CG_THREADS + threadIdx.x;
     const uint32_t stride = P.bpg * CG_THREADS;
     double *x = G.x, *r = G.r, *z = G.z;
+    const bool halo = G.zpeer[0] != nullptr;  // multi-slab run: ghost-plane exchange
+    // pointers come from shared memory: tell the compiler they are global
+    // (LDG/STG instead of generic LD/ST)
+    __builtin_assume(__isGlobal(x));
+    __builtin_assume(__isGlobal(r));
+    __builtin_assume(__isGlobal(z));
     const double inv_h = P.inv_h, inv_h2 = P.inv_h2;
 
     // ---- setup (krylov.py:102-119): project rhs; r = op(x0) - rhs; z = M^-1 r;
@@ -324,7 +351,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
             const double zi = __dmul_rn(ri, jacobi_inv<OP>(rc, T));
             r[i] = ri;
             z[i] = zi;
-            halo_store(G, OP == 0 ? rec_comp(rc) : fam_p, i, zi);
+            if (halo) halo_store(G, OP == 0 ? rec_comp(rc) : fam_p, i, zi);
             v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
             v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
             v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
@@ -347,6 +374,8 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
     int64_t sat = 0, its = 0;
     bool conv = (ref == 0.0);
     double *dold = G.d0, *dnew = G.d1;
+    __builtin_assume(__isGlobal(dold));
+    __builtin_assume(__isGlobal(dnew));
     unsigned long long ph[4] = {0, 0, 0, 0};  // this block's phase sums (thread 0)
     if (!conv) {
         for (int64_t it = 0; it < P.max_iter; ++it) {
@@ -429,7 +458,7 @@ __global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
                 x[i] = xi;
                 r[i] = ri;
                 z[i] = zi;
-                halo_store(G, OP == 0 ? rec_comp(rc) : fam_p, i, zi);
+                if (halo) halo_store(G, OP == 0 ? rec_comp(rc) : fam_p, i, zi);
                 v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
                 v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
                 v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
