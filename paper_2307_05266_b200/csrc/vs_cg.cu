@@ -73,13 +73,16 @@ __device__ __forceinline__ double op_value(uint64_t rc, double vi, const double 
         for (int s = 1; s < 2 * DIM; ++s) acc = __dadd_rn(acc, vn[s]);
         return __dsub_rn(__dmul_rn(T.diag[rec_vcode(rc)], vi), __dmul_rn(inv_h2, acc));
     } else {
+        // branch-free: an absent face has code 0 and invA[0] = 0.0, so its
+        // weight is (finite) * 0.0 = +-0.0 -- the reference's padded 0.0 up to
+        // the sign of zero (neighbour values of absent faces are finite: the
+        // gather is clamped to the DOF itself)
         double out = 0.0;
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
             // slot 2a = +e_a neighbour (out face), 2a+1 = -e_a neighbour (in face)
-            const int ci = rec_pin(rc, a), co = rec_pout(rc, a);
-            const double wi = ci ? __dmul_rn(__dmul_rn(__dsub_rn(vi, vn[2 * a + 1]), inv_h), T.invA[ci]) : 0.0;
-            const double wo = co ? __dmul_rn(__dmul_rn(__dsub_rn(vn[2 * a], vi), inv_h), T.invA[co]) : 0.0;
+            const double wi = __dmul_rn(__dmul_rn(__dsub_rn(vi, vn[2 * a + 1]), inv_h), T.invA[rec_pin(rc, a)]);
+            const double wo = __dmul_rn(__dmul_rn(__dsub_rn(vn[2 * a], vi), inv_h), T.invA[rec_pout(rc, a)]);
             out = __dadd_rn(out, __dsub_rn(wi, wo));
         }
         return __dmul_rn(out, inv_h);
