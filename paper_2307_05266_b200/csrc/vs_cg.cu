@@ -23,36 +23,41 @@
 
 namespace vs {
 
-__device__ __forceinline__ uint32_t rank_of(const uint2 *__restrict__ meta, int nw, int L, int z) {
-    const uint2 m = __ldg(meta + (L * nw + (z >> 5)));
-    const uint32_t b = (uint32_t)z & 31u;
-    const uint32_t rk = m.y + (uint32_t)__popc(m.x & ((1u << b) - 1u));
-    return ((m.x >> b) & 1u) ? rk : ABSENT;
-}
 
 // ranks of the 2*DIM neighbours in the reference slot order
 // (x+, x-, [y+, y-,] z+, z-)   (operators.py:269-271: d = 0..dim-1, s = +1, -1)
 // (nx = extent of the local x axis: n for a whole-domain group, slab planes
-// + 2 ghost planes otherwise -- owned DOFs of a slab never wrap in x)
+// + 2 ghost planes otherwise -- owned DOFs of a slab never wrap in x).
+// The tangential neighbours share the DOF's bit position, so their ranks are
+// word + popc(mask & below(b)) at a word offset from the DOF's own word.
 template <int DIM>
 __device__ __forceinline__ void neighbour_ranks(const uint2 *__restrict__ meta, int nw, int n, int nx,
                                                 uint64_t rc, uint32_t (&nr)[2 * DIM]) {
     const int z = rec_z(rc), y = rec_y(rc), x = rec_x(rc);
-    const int sx = DIM == 3 ? n : 1;
-    const int L = DIM == 3 ? x * n + y : x;
-    const int Lxp = (x == nx - 1) ? L - (nx - 1) * sx : L + sx;
-    const int Lxm = (x == 0) ? L + (nx - 1) * sx : L - sx;
-    nr[0] = rank_of(meta, nw, Lxp, z);
-    nr[1] = rank_of(meta, nw, Lxm, z);
+    const uint32_t b = (uint32_t)z & 31u, below = (1u << b) - 1u;
+    const int lineW = (DIM == 3 ? x * n + y : x) * nw;  // word 0 of the DOF's line
+    const int w0 = lineW + (z >> 5);
+    const int planeW = (DIM == 3 ? n : 1) * nw;           // words per x-plane
+    auto tang = [&](int idx) -> uint32_t {
+        const uint2 m = __ldg(meta + idx);
+        const uint32_t rk = m.y + (uint32_t)__popc(m.x & below);
+        return ((m.x >> b) & 1u) ? rk : ABSENT;
+    };
+    nr[0] = tang(w0 + ((x == nx - 1) ? -(nx - 1) * planeW : planeW));
+    nr[1] = tang(w0 + ((x == 0) ? (nx - 1) * planeW : -planeW));
     if (DIM == 3) {
-        const int Lyp = (y == n - 1) ? L - (n - 1) : L + 1;
-        const int Lym = (y == 0) ? L + (n - 1) : L - 1;
-        nr[2] = rank_of(meta, nw, Lyp, z);
-        nr[3] = rank_of(meta, nw, Lym, z);
+        nr[2] = tang(w0 + ((y == n - 1) ? -(n - 1) * nw : nw));
+        nr[3] = tang(w0 + ((y == 0) ? (n - 1) * nw : -nw));
     }
     const int zp = (z == n - 1) ? 0 : z + 1, zm = (z == 0) ? n - 1 : z - 1;
-    nr[2 * DIM - 2] = rank_of(meta, nw, L, zp);
-    nr[2 * DIM - 1] = rank_of(meta, nw, L, zm);
+    auto along = [&](int zz) -> uint32_t {
+        const uint2 m = __ldg(meta + lineW + (zz >> 5));
+        const uint32_t bb = (uint32_t)zz & 31u;
+        const uint32_t rk = m.y + (uint32_t)__popc(m.x & ((1u << bb) - 1u));
+        return ((m.x >> bb) & 1u) ? rk : ABSENT;
+    };
+    nr[2 * DIM - 2] = along(zp);
+    nr[2 * DIM - 1] = along(zm);
 }
 
 struct Tabs {
