@@ -286,9 +286,21 @@ class PcgOut:
     converged: bool
 
 
+def _exact_dot(a, b):
+    import math
+
+    return math.fsum(np.asarray(a) * np.asarray(b))
+
+
+# dot product used by pcg: the reference's (numpy/BLAS) or, for the parity
+# tests' rounding-sensitivity probe, an exactly rounded one (math.fsum)
+_DOT = [lambda a, b: float(a @ b)]
+
+
 def pcg(op, prec, rhs, x0=None, tol=1e-6, norm_kind="preconditioned",
         max_iter=10000, project=False, record=True, step_hook=None) -> PcgOut:
     """Preconditioned CG with r = op(x) - rhs, x -= alpha d (krylov.py:76-182)."""
+    dot = _DOT[0]
     rhs = np.array(rhs, dtype=float)
     x = np.zeros_like(rhs) if x0 is None else np.array(x0, dtype=float)
     if prec is None:
@@ -301,15 +313,15 @@ def pcg(op, prec, rhs, x0=None, tol=1e-6, norm_kind="preconditioned",
     z = prec(r)
     if project:
         z = z - z.mean()
-    rp = [float(np.linalg.norm(z))]
-    ru = [float(np.linalg.norm(r))]
+    rp = [float(np.sqrt(dot(z, z)))]
+    ru = [float(np.sqrt(dot(r, r)))]
     ref = rp[0] if use_prec else ru[0]
     alphas, betas = [], []
     its = 0
     conv = ref == 0.0
     if not conv:
         d = z.copy()
-        rz = float(r @ z)
+        rz = dot(r, z)
         for k in range(max_iter):
             if rz < 0.0:
                 raise RuntimeError(
@@ -318,7 +330,7 @@ def pcg(op, prec, rhs, x0=None, tol=1e-6, norm_kind="preconditioned",
                 conv = True
                 break
             q = op(d)
-            dq = float(d @ q)
+            dq = dot(d, q)
             if dq <= 0.0:
                 raise RuntimeError(
                     f"operator not SPD on subspace: d'q = {dq:.3e} at iteration {k}")
@@ -330,11 +342,11 @@ def pcg(op, prec, rhs, x0=None, tol=1e-6, norm_kind="preconditioned",
             z = prec(r)
             if project:
                 z = z - z.mean()
-            rz_new = float(r @ z)
+            rz_new = dot(r, z)
             beta = rz_new / rz
             rz = rz_new
-            nz = float(np.linalg.norm(z))
-            nr = float(np.linalg.norm(r))
+            nz = float(np.sqrt(dot(z, z)))
+            nr = float(np.sqrt(dot(r, r)))
             if not (np.isfinite(nz) and np.isfinite(nr)):
                 raise RuntimeError(f"non-finite residual at iteration {k + 1}")
             alphas.append(alpha)
@@ -403,7 +415,21 @@ def solve_simple(sys, r, eps, inv_s=None):
 
 def solve_schur(sys: OracleSystem, prec="simple", eps_S=1e-3,
                 outer_norm="preconditioned", eps_A=1e-6, eps_Shat=1e-6,
-                max_iter=1000, k_ref=None) -> dict:
+                max_iter=1000, k_ref=None, exact_dots=False) -> dict:
+    """Outer PCG on S p = g (schur.py:291-385); exact_dots=True re-runs the
+    same algorithm with exactly rounded dot products (rounding-sensitivity
+    probe for the parity tests)."""
+    if exact_dots:
+        old = _DOT[0]
+        _DOT[0] = _exact_dot
+        try:
+            return solve_schur(sys, prec, eps_S, outer_norm, eps_A, eps_Shat, max_iter, k_ref)
+        finally:
+            _DOT[0] = old
+    return _solve_schur(sys, prec, eps_S, outer_norm, eps_A, eps_Shat, max_iter, k_ref)
+
+
+def _solve_schur(sys, prec, eps_S, outer_norm, eps_A, eps_Shat, max_iter, k_ref) -> dict:
     """Outer PCG on S p = g with velocity iterate and refresh (schur.py:291-385).
 
     Returns a dict with the SolveReport fields (plus ``uf_iters``, the

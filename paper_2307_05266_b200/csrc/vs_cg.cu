@@ -290,7 +290,7 @@ __device__ __forceinline__ void fetch_dof(const CgParams &P, const CgGroup &G, c
 }
 
 template <int DIM, int OP, int TIER>
-__global__ void __launch_bounds__(CG_THREADS, 2) k_pcg(const CgParams P) {
+__global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
     extern __shared__ __align__(16) uint8_t dyn_smem[];

@@ -8,7 +8,7 @@
 
 namespace vs {
 
-constexpr int CG_THREADS = 512;
+constexpr int CG_THREADS = 1024;
 constexpr int RED_THREADS = 256;
 constexpr int RED_MAX_BLOCKS = 592;
 constexpr int VS_MAX_SLABS = 16;
@@ -88,7 +88,7 @@ void launch_vec(int kind, double *out, double *a, const double *b, double sc, in
 void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s);
 int launch_reduce(int kind, const double *a, const double *b, int64_t m, double *part, double *out,
                   cudaStream_t s);
-constexpr size_t CG_SMEM_BUDGET = 108 * 1024;  // dynamic smem per block (2 blocks / SM)
+constexpr size_t CG_SMEM_BUDGET = 200 * 1024;  // dynamic smem per block (1 block / SM)
 struct CgPlan {
     int tier, grid;
     uint32_t slots;
