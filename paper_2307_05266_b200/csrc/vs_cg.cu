@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
         rp0 = sqrt(v[1]);
         ru0 = sqrt(v[2]);
     }
-    const double ref = P.norm_prec ? rp0 : ru0;
+    const double ref = rp0;  // inner solves: preconditioned norm (schur.py:207-210, :259-262)
     double beta = 0.0, rp_last = rp0, ru_last = ru0, sval = 0.0;
     int status = 0;
     int64_t sat = 0, its = 0;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
             if (rz < 0.0) { status = 1; sval = rz; sat = it; break; }
             if (rz == 0.0) { conv = true; break; }
             const bool first = (it == 0);
-            const uint64_t t0 = P.phase_ns ? gtimer() : 0;
+            const uint64_t t0 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             // ---- P1: d = z - mu + beta d_old, q = op(d), d.q
             double v1[1] = {0.0};
             uint32_t k = 0;
@@ -433,14 +433,21 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                 if (PROJ) zc = __dsub_rn(zc, mu);
                 dnew[i] = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dold[i]));
             }
-            const uint64_t t1 = P.phase_ns ? gtimer() : 0;
+            const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             grid_sum<1>(v1, P.part + 16 * gridDim.x, P.bar, gen, s_warp, s_tot);
-            const uint64_t t2 = P.phase_ns ? gtimer() : 0;
+            const uint64_t t2 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             const double dq = v1[0];
             if (dq <= 0.0) { status = 2; sval = dq; sat = it; break; }
             const double alpha = rz / dq;
             // ---- P2: q = op(d); x -= alpha d; r -= alpha q; z = M^-1 r; sums
-            double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            // per-iteration sums: r.z, z.z (+ sum z, sum r when projected).
+            // Inner solves stop on the preconditioned norm (schur.py:207-210),
+            // so |r| is not needed: z = r * (positive finite inverse diagonal)
+            // is non-finite exactly when r is, which keeps krylov.py:159-160.
+            constexpr int KL = PROJ ? 4 : 2;
+            double v[KL];
+#pragma unroll
+            for (int q = 0; q < KL; ++q) v[q] = 0.0;
             k = 0;
             for (uint32_t i = tid; i < m; i += stride, ++k) {
                 const uint32_t ip = i + P.pf_dist * stride;
@@ -469,12 +476,13 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                 if (halo) halo_store(G, OP == 0 ? rec_comp(rc) : fam_p, i, zi);
                 v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
                 v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
-                v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
-                v[3] = __dadd_rn(v[3], zi);
-                v[4] = __dadd_rn(v[4], ri);
+                if (PROJ) {
+                    v[2] = __dadd_rn(v[2], zi);
+                    v[3] = __dadd_rn(v[3], ri);
+                }
             }
-            const uint64_t t3 = P.phase_ns ? gtimer() : 0;
-            grid_sum<5>(v, P.part + 24 * gridDim.x, P.bar, gen, s_warp, s_tot);
+            const uint64_t t3 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
+            grid_sum<KL>(v, P.part + 24 * gridDim.x, P.bar, gen, s_warp, s_tot);
             if (P.phase_ns && threadIdx.x == 0) {
                 const uint64_t t4 = gtimer();
                 ph[0] += t1 - t0;
@@ -483,20 +491,19 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                 ph[3] += t4 - t3;
             }
             if (PROJ) {
-                mu = v[3] / P.m_global;
-                v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
-                v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
+                mu = v[2] / P.m_global;
+                v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[3]));
+                v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[2]));
             }
             const double rz_new = v[0];
             beta = rz_new / rz;
             rz = rz_new;
-            const double nz = sqrt(v[1]), nrr = sqrt(v[2]);
-            if (!(isfinite(nz) && isfinite(nrr))) { status = 3; sat = it + 1; break; }
+            const double nz = sqrt(v[1]);
+            if (!isfinite(nz)) { status = 3; sat = it + 1; break; }
             its = it + 1;
             rp_last = nz;
-            ru_last = nrr;
             double *t = dold; dold = dnew; dnew = t;
-            if ((P.norm_prec ? nz : nrr) / ref < P.tol) { conv = true; break; }
+            if (nz / ref < P.tol) { conv = true; break; }
         }
     }
     if (P.phase_ns && threadIdx.x == 0) {  // [0..3] block 0, [4..7] max, [8..11] sum over blocks

@@ -7,7 +7,9 @@ import time
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("VOXSCHUR_PHASE_TIMING", "1")
+if "--no-phases" not in sys.argv:
+    os.environ.setdefault("VOXSCHUR_PHASE_TIMING", "1")
+sys.argv = [a for a in sys.argv if a != "--no-phases"]
 import paper_2307_05266_b200 as vx  # noqa: E402
 from paper_2307_05266_b200 import _lib  # noqa: E402
 from paper_2307_05266_b200 import configs, schur  # noqa: E402
