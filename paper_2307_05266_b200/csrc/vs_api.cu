@@ -106,6 +106,14 @@ struct vs_ctx {
     unsigned long long *phase_ns = nullptr;  // VOXSCHUR_PHASE_TIMING=1
     double *part = nullptr, *red_part = nullptr, *scal = nullptr;
     CgOut *cgout = nullptr;
+    // async inner solves: CgOut log + event pool (read back once per outer iteration)
+    CgOut *cglog = nullptr, *h_cglog = nullptr;
+    int ncglog = 0, cglog_cap = 0;
+    std::vector<cudaEvent_t> evpool;
+    std::vector<int> log_op;
+    OuterState *ost = nullptr, *h_ost = nullptr;
+    double *hist = nullptr;
+    int64_t hist_cap = 0;
     double *h_scal = nullptr;  // pinned
     CgOut *h_cg = nullptr;     // pinned
     CgPlan plan_A{}, plan_S{};
@@ -135,6 +143,9 @@ struct vs_ctx {
         if (h_scal) cudaFreeHost(h_scal);
         if (h_cg) cudaFreeHost(h_cg);
         if (h_groups) cudaFreeHost(h_groups);
+        if (h_cglog) cudaFreeHost(h_cglog);
+        if (h_ost) cudaFreeHost(h_ost);
+        for (cudaEvent_t e : evpool) cudaEventDestroy(e);
         for (cudaEvent_t e : {ev0, ev1, evs0, evs1})
             if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
@@ -153,7 +164,6 @@ struct vs_ctx {
             const double *pb = b < 0 ? nullptr : (space == 0 ? S.u[b] : S.p[b]);
             int64_t off = 0, m = S.m_own[space];
             if (lo_fam >= 0) { off = S.own_off[lo_fam]; m = S.own[lo_fam]; }
-            if (m == 0) continue;
             launches += launch_reduce(kind, pa + off, pb ? pb + off : nullptr, m, red_part, scal + s, stream);
         }
         CK(cudaMemcpyAsync(h_scal, scal, R * sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -164,12 +174,24 @@ struct vs_ctx {
     double dot(int space, int a, int b) { return reduce(space, 1, a, b); }
     double sum(int space, int a) { return reduce(space, 0, a, -1); }
     double mean(int space, int a) { return sum(space, a) / (double)(space == 0 ? m_u : m_p); }
-    void vec(int space, int kind, int out, int a, int b, double sc) {
+    void vec(int space, int kind, int out, int a, int b, double sc, const double *sp = nullptr) {
         for (int s = 0; s < R; ++s) {
             Slab &S = slabs[s];
             double **v = space == 0 ? S.u : S.p;
-            launch_vec(kind, out < 0 ? nullptr : v[out], v[a], b < 0 ? nullptr : v[b], sc, S.m_own[space], stream);
+            launch_vec(kind, out < 0 ? nullptr : v[out], v[a], b < 0 ? nullptr : v[b], sc, sp, S.m_own[space],
+                       stream);
             ++launches;
+        }
+    }
+    // device-resident reduction into slot q (scal[q*R + s]); no host sync
+    void reduce_dev(int space, int kind, int a, int b, int q, int64_t lo_fam = -1) {
+        for (int s = 0; s < R; ++s) {
+            Slab &S = slabs[s];
+            const double *pa = space == 0 ? S.u[a] : S.p[a];
+            const double *pb = b < 0 ? nullptr : (space == 0 ? S.u[b] : S.p[b]);
+            int64_t off = 0, m = S.m_own[space];
+            if (lo_fam >= 0) { off = S.own_off[lo_fam]; m = S.own[lo_fam]; }
+            launches += launch_reduce(kind, pa + off, pb ? pb + off : nullptr, m, red_part, scal + q * R + s, stream);
         }
     }
     void copy(int space, int dst, int src) {
@@ -343,17 +365,29 @@ Status cg_status_to_error(const CgOut &o, int which) {
     return {VS_OK, ""};
 }
 
-// One fused device PCG solve over all slabs (one cooperative launch).
-// op 0: velocity A (x0 allowed), op 1: S_hat (projected).  Slots index the
-// slab vectors.  Returns the iteration count; throws Status on errors.
-int64_t cg_solve(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
+constexpr int GROUP_RING = 8;  // group-table staging slots (>= launches between syncs)
+
+// Launch one fused device PCG solve over all slabs (one cooperative launch)
+// without waiting: its CgOut goes to log slot c->ncglog (returned), its
+// launch time to an event pair of the pool.  op 0: velocity A (x0
+// allowed), op 1: S_hat (projected).  Slots index the slab vectors.
+int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     const int64_t m = op == 0 ? c->m_u : c->m_p;
-    if (m == 0) return 0;
     const int R = c->R;
+    if (c->ncglog >= c->cglog_cap) throw Status{VS_ECUDA, "inner-solve log overflow"};
+    const int li = c->ncglog++;
+    c->log_op.resize(c->ncglog);
+    c->log_op[li] = op;
+    if (m == 0) {
+        CK(cudaMemsetAsync(c->cglog + li, 0, sizeof(CgOut), c->stream));
+        return li;
+    }
     if (x0 >= 0) c->halo(op == 0 ? 0 : 1, x0);  // A x0 needs x0 on the ghost planes
+    const int ring = li % GROUP_RING;
+    CgGroup *hg = c->h_groups + ring * R;
     for (int s = 0; s < R; ++s) {
         Slab &S = c->slabs[s];
-        CgGroup &G = c->h_groups[s];
+        CgGroup &G = hg[s];
         memset(&G, 0, sizeof G);
         double **v = op == 0 ? S.u : S.p;
         if (op == 0) {
@@ -388,10 +422,11 @@ int64_t cg_solve(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
             }
         }
     }
-    CK(cudaMemcpyAsync(c->d_groups, c->h_groups, R * sizeof(CgGroup), cudaMemcpyHostToDevice, c->stream));
+    CgGroup *dg = c->d_groups + ring * R;
+    CK(cudaMemcpyAsync(dg, hg, R * sizeof(CgGroup), cudaMemcpyHostToDevice, c->stream));
     CgParams P;
     memset(&P, 0, sizeof P);
-    P.groups = c->d_groups;
+    P.groups = dg;
     P.group_base = 0;
     P.n = c->n;
     P.nw = c->nw;
@@ -399,7 +434,7 @@ int64_t cg_solve(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.part = c->part;
     P.bar = c->bar;
     P.phase_ns = c->phase_ns;
-    P.out = c->cgout;
+    P.out = c->cglog + li;
     P.tol = eps;
     P.max_iter = std::max<int64_t>(1000, 2 * m);  // schur.py:196-197
     P.norm_prec = 1;
@@ -413,23 +448,59 @@ int64_t cg_solve(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     const CgPlan &pl = op == 0 ? c->plan_A : c->plan_S;
     CK(cudaMemsetAsync(c->bar, 0, sizeof(unsigned), c->stream));
     ++c->launches;
-    CK(cudaEventRecord(c->evs0, c->stream));
+    while ((int)c->evpool.size() < 2 * c->ncglog) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->evpool.push_back(e);
+    }
+    CK(cudaEventRecord(c->evpool[2 * li], c->stream));
     CK(launch_pcg(c->dim, op, pl, R, P, c->stream));
-    CK(cudaEventRecord(c->evs1, c->stream));
+    CK(cudaEventRecord(c->evpool[2 * li + 1], c->stream));
     ++c->launches;
-    CK(cudaMemcpyAsync(c->h_cg, c->cgout, sizeof(CgOut), cudaMemcpyDeviceToHost, c->stream));
+    return li;
+}
+
+// After a host sync: account the logged inner solves [from, ncglog) and
+// raise the first failure in program order.  Returns the iteration sum per op.
+void drain_log(vs_ctx *c, int from, int64_t *its_op) {
+    const int n = c->ncglog - from;
+    if (n <= 0) return;
+    for (int li = from; li < c->ncglog; ++li) {
+        const CgOut &o = c->h_cglog[li];
+        const int op = c->log_op[li];
+        const int64_t m = op == 0 ? c->m_u : c->m_p;
+        float ms = 0;
+        if (m) CK(cudaEventElapsedTime(&ms, c->evpool[2 * li], c->evpool[2 * li + 1]));
+        vs_kstat &st = op == 0 ? c->st_A : c->st_S;
+        st.launches += m ? 1 : 0;
+        st.iterations += o.iterations;
+        st.dof_iters += o.iterations * m;
+        st.ms += ms;
+        if (its_op) its_op[li - from] = o.iterations;
+        if (m) {
+            Status s = cg_status_to_error(o, op);
+            if (s.code != VS_OK) throw s;
+        }
+    }
+}
+
+// fetch log slots [from, ncglog) to the host (async, before a sync)
+void fetch_log(vs_ctx *c, int from) {
+    const int n = c->ncglog - from;
+    if (n > 0)
+        CK(cudaMemcpyAsync(c->h_cglog + from, c->cglog + from, n * sizeof(CgOut), cudaMemcpyDeviceToHost, c->stream));
+}
+
+// Synchronous inner solve: returns the iteration count; throws on errors.
+int64_t cg_solve(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
+    c->ncglog = 0;
+    cg_async(c, op, rhs, x0, eps, x);
+    fetch_log(c, 0);
     c->sync();
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, c->evs0, c->evs1));
-    const CgOut o = *c->h_cg;
-    vs_kstat &st = op == 0 ? c->st_A : c->st_S;
-    st.launches += 1;
-    st.iterations += o.iterations;
-    st.dof_iters += o.iterations * m;
-    st.ms += ms;
-    Status s = cg_status_to_error(o, op);
-    if (s.code != VS_OK) throw s;
-    return o.iterations;
+    int64_t its = 0;
+    drain_log(c, 0, &its);
+    c->ncglog = 0;
+    return its;
 }
 
 void reset_stats(vs_ctx *c) {
@@ -567,11 +638,16 @@ void build_slabs(vs_ctx *C, int R) {
     C->plan_A = pcg_plan(dim, 0, mu_max, R, C->device);
     C->plan_S = pcg_plan(dim, 1, mp_max, R, C->device);
     C->part = C->alloc<double>((size_t)4 * 8 * R * std::max(C->plan_A.grid, C->plan_S.grid));
-    C->d_groups = C->alloc<CgGroup>(R);
-    CK(cudaMallocHost(&C->h_groups, R * sizeof(CgGroup)));
-    C->scal = C->alloc<double>(std::max(8, R));
+    C->d_groups = C->alloc<CgGroup>(R * GROUP_RING);
+    CK(cudaMallocHost(&C->h_groups, R * GROUP_RING * sizeof(CgGroup)));
+    C->scal = C->alloc<double>(std::max(8, Q_COUNT * R));
     CK(cudaFreeHost(C->h_scal));
-    CK(cudaMallocHost(&C->h_scal, std::max(8, R) * sizeof(double)));
+    CK(cudaMallocHost(&C->h_scal, std::max(8, Q_COUNT * R) * sizeof(double)));
+    C->cglog_cap = 16;
+    C->cglog = C->alloc<CgOut>(C->cglog_cap);
+    CK(cudaMallocHost(&C->h_cglog, C->cglog_cap * sizeof(CgOut)));
+    C->ost = C->alloc<OuterState>(1);
+    CK(cudaMallocHost(&C->h_ost, sizeof(OuterState)));
 }
 
 }  // namespace
@@ -916,6 +992,11 @@ int vs_solve_simple(vs_ctx *c, const double *r, double eps, double *z, int64_t *
 }
 
 // ------------------------------------------------------------ solve_schur
+// The outer PCG (krylov.py:76-182) over S = B A^-1 B^T with the SIMPLE or
+// identity preconditioner (schur.py:291-385).  Every vector op, reduction
+// and scalar update runs on the device in the reference's order; the host
+// enqueues one outer iteration and synchronises once at its end to read the
+// scalar state (convergence / error flags) and the inner-solve log.
 
 int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double *velocity, vs_report *rep,
                    double *res_prec, double *res_unprec, double *perm_history, double *alpha_out,
@@ -926,121 +1007,185 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
         reset_stats(c);
         memset(rep, 0, sizeof *rep);
         cudaStream_t s = c->stream;
+        const int R = c->R;
+        const int use_prec = cfg->outer_norm == 0;
+        // device histories: alpha, beta, res_prec, res_unprec, perm (stride max_iter + 2)
+        const int64_t hs = cfg->max_iter + 2;
+        if (hs > c->hist_cap) {
+            c->hist = c->alloc<double>(5 * hs);
+            c->hist_cap = hs;
+        }
+        OuterState init{};
+        init.hstride = hs;
+        CK(cudaMemcpyAsync(c->ost, &init, sizeof init, cudaMemcpyHostToDevice, s));
+        double *mu = &c->ost->mu, *alpha = &c->ost->alpha, *beta = &c->ost->beta;
         CK(cudaEventRecord(c->ev0, s));
-        auto perm = [&](int slot) {  // schur.py:288
-            return cfg->h_pow_dim * c->reduce(0, 0, slot, -1, c->flow_dir);
+        auto perm = [&](int slot, int64_t k) {  // schur.py:288 -> hist perm[k + 1]
+            c->reduce_dev(0, 0, slot, -1, Q_PERM, c->flow_dir);
+            launch_outer(SO_PERM, c->ost, c->scal, R, cfg->h_pow_dim, k, 0, 0, c->hist, s);
+            ++c->launches;
+        };
+        auto mean_into_mu = [&](int slot) {
+            c->reduce_dev(1, 0, slot, -1, Q_MU);
+            launch_outer(SO_MEAN, c->ost, c->scal, R, (double)c->m_p, 0, 0, 0, c->hist, s);
+            ++c->launches;
         };
         int64_t tot_vel = 0, tot_pre = 0;
-        // g, u_f = schur_rhs (schur.py:228-231, :308)
+        std::vector<int> vel_logs;  // log slots counted in inner_iter_totals["velocity"]
+        // drain the log + state after a sync; raise the first failure in program order
+        auto settle = [&](int failure_stage_state) {
+            fetch_log(c, 0);
+            CK(cudaMemcpyAsync(c->h_ost, c->ost, sizeof(OuterState), cudaMemcpyDeviceToHost, s));
+            c->sync();
+            std::vector<int64_t> its(c->ncglog);
+            // inner failures and outer flags interleave in program order: the
+            // velocity solve precedes d'q, the preconditioner solve precedes
+            // the r'z / norm checks
+            for (int li = 0; li < c->ncglog; ++li) {
+                const OuterState &o = *c->h_ost;
+                if (c->log_op[li] == 1 && o.status == 2) break;  // d'q failed before the S_hat solve
+                (void)failure_stage_state;
+                const int save = c->ncglog;
+                c->ncglog = li + 1;
+                drain_log(c, li, &its[li]);
+                c->ncglog = save;
+            }
+            for (int li = 0; li < c->ncglog; ++li) {
+                if (c->log_op[li] == 0) tot_vel += its[li];
+                else tot_pre += its[li];
+            }
+            const OuterState &o = *c->h_ost;
+            char buf[256];
+            if (o.status == 1) {
+                snprintf(buf, sizeof buf, "preconditioner not SPD on subspace: r'z = %.3e at iteration %lld", o.value,
+                         (long long)o.at);
+                throw Status{VS_ERUNTIME, buf};
+            }
+            if (o.status == 2) {
+                snprintf(buf, sizeof buf, "operator not SPD on subspace: d'q = %.3e at iteration %lld", o.value,
+                         (long long)o.at);
+                throw Status{VS_ERUNTIME, buf};
+            }
+            if (o.status == 3) {
+                snprintf(buf, sizeof buf, "non-finite residual at iteration %lld", (long long)o.at);
+                throw Status{VS_ERUNTIME, buf};
+            }
+            c->ncglog = 0;
+        };
+        // g, u_f = schur_rhs (schur.py:228-231, :308); the u_f solve is not counted (:230)
+        c->ncglog = 0;
         c->force(U_RHS, -1);
-        rep->uf_iters = cg_solve(c, 0, U_RHS, -1, cfg->eps_A, U_F);
+        cg_async(c, 0, U_RHS, -1, cfg->eps_A, U_F);
         c->div(U_F, P_B);  // g -> P_B
         // outer_op(p) = B A^-1 B^T p, last_w kept (schur.py:312-316)
         auto outer_op = [&](int p, int q) {
             c->grad(p, U_RHS);
-            tot_vel += cg_solve(c, 0, U_RHS, -1, cfg->eps_A, U_W);
+            cg_async(c, 0, U_RHS, -1, cfg->eps_A, U_W);
             c->div(U_W, q);
         };
-        // z = prec(r); z -= mean(z)   (schur.py:324-327, krylov.py:117-119)
+        // z = prec(r); z -= mean(z)   (schur.py:324-327, krylov.py:117-119, :151-153)
         auto outer_prec = [&](int r, int z) {
             if (cfg->prec == 1) {
-                tot_pre += cg_solve(c, 1, r, -1, cfg->eps_Shat, P_TMP);
-                const double m = c->mean(1, P_TMP);
-                c->vec(1, 0, z, P_TMP, -1, m);
+                cg_async(c, 1, r, -1, cfg->eps_Shat, P_TMP);
+                mean_into_mu(P_TMP);
+                c->vec(1, 0, z, P_TMP, -1, 0.0, mu);
             } else {
-                const double m = c->mean(1, r);
-                c->vec(1, 0, z, r, -1, m);
+                mean_into_mu(r);
+                c->vec(1, 0, z, r, -1, 0.0, mu);
             }
+        };
+        auto norms = [&]() {  // r.z, z.z, r.r (krylov.py:141, :154-158)
+            c->reduce_dev(1, 1, P_R, P_Z, Q_RZ);
+            c->reduce_dev(1, 1, P_Z, P_Z, Q_ZZ);
+            c->reduce_dev(1, 1, P_R, P_R, Q_RR);
         };
         // u = u_f.copy(); perm_history = [k(u)]
         c->copy(0, U_ITER, U_F);
-        std::vector<double> ph, rp, ru, al, be;
-        ph.push_back(perm(U_ITER));
-        // ---- outer pcg (krylov.py:76-182) with project_nullspace=True
-        const bool use_prec = cfg->outer_norm == 0;
-        {
-            const double mg = c->mean(1, P_B);
-            c->vec(1, 0, P_B, P_B, -1, mg);  // rhs -= mean(rhs)
-            for (auto &S : c->slabs)          // x = 0 (- mean 0)
-                CK(cudaMemsetAsync(S.p[P_X], 0, S.m_all[1] * sizeof(double), s));
-        }
+        perm(U_ITER, -1);
+        // ---- outer pcg setup with project_nullspace=True (krylov.py:102-128)
+        mean_into_mu(P_B);
+        c->vec(1, 0, P_B, P_B, -1, 0.0, mu);  // rhs -= mean(rhs)
+        for (auto &S : c->slabs) CK(cudaMemsetAsync(S.p[P_X], 0, S.m_all[1] * sizeof(double), s));  // x = 0
         outer_op(P_X, P_Q);
         c->vec(1, 4, P_R, P_Q, P_B, 0.0);  // r = op(x) - rhs
         outer_prec(P_R, P_Z);
-        rp.push_back(std::sqrt(c->dot(1, P_Z, P_Z)));
-        ru.push_back(std::sqrt(c->dot(1, P_R, P_R)));
-        const double ref = use_prec ? rp[0] : ru[0];
-        bool conv = ref == 0.0;
-        int64_t its = 0;
-        if (!conv) {
-            c->copy(1, P_D, P_Z);
-            double rz = c->dot(1, P_R, P_Z);
-            char buf[256];
-            for (int64_t k = 0; k < cfg->max_iter; ++k) {
-                if (rz < 0.0) {
-                    snprintf(buf, sizeof buf, "preconditioner not SPD on subspace: r'z = %.3e at iteration %lld", rz,
-                             (long long)k);
-                    throw Status{VS_ERUNTIME, buf};
-                }
-                if (rz == 0.0) { conv = true; break; }
-                outer_op(P_D, P_Q);
-                const double dq = c->dot(1, P_D, P_Q);
-                if (dq <= 0.0) {
-                    snprintf(buf, sizeof buf, "operator not SPD on subspace: d'q = %.3e at iteration %lld", dq,
-                             (long long)k);
-                    throw Status{VS_ERUNTIME, buf};
-                }
-                const double alpha = rz / dq;
-                c->vec(1, 1, -1, P_X, P_D, alpha);    // x -= alpha d
-                c->vec(1, 1, -1, P_R, P_Q, alpha);    // r -= alpha q
-                c->vec(0, 2, -1, U_ITER, U_W, alpha);  // u += alpha w (schur.py:334-336)
-                ph.push_back(perm(U_ITER));
-                outer_prec(P_R, P_Z);
-                const double rz_new = c->dot(1, P_R, P_Z);
-                const double beta = rz_new / rz;
-                rz = rz_new;
-                const double nz = std::sqrt(c->dot(1, P_Z, P_Z));
-                const double nr = std::sqrt(c->dot(1, P_R, P_R));
-                if (!(std::isfinite(nz) && std::isfinite(nr))) {
-                    snprintf(buf, sizeof buf, "non-finite residual at iteration %lld", (long long)(k + 1));
-                    throw Status{VS_ERUNTIME, buf};
-                }
-                al.push_back(alpha);
-                be.push_back(beta);
-                rp.push_back(nz);
-                ru.push_back(nr);
-                its = k + 1;
-                if ((use_prec ? nz : nr) / ref < cfg->eps_S) { conv = true; break; }
-                c->vec(1, 3, P_D, P_D, P_Z, beta);  // d = z + beta d
+        norms();
+        launch_outer(SO_INIT, c->ost, c->scal, R, 0, 0, cfg->eps_S, use_prec, c->hist, s);
+        ++c->launches;
+        c->copy(1, P_D, P_Z);
+        {
+            // the u_f solve (log slot 0) is discarded from the totals
+            fetch_log(c, 0);
+            CK(cudaMemcpyAsync(c->h_ost, c->ost, sizeof(OuterState), cudaMemcpyDeviceToHost, s));
+            c->sync();
+            int64_t its[16] = {0};
+            drain_log(c, 0, its);
+            rep->uf_iters = its[0];
+            for (int li = 1; li < c->ncglog; ++li) {
+                if (c->log_op[li] == 0) tot_vel += its[li];
+                else tot_pre += its[li];
+            }
+            c->ncglog = 0;
+            const OuterState &o = *c->h_ost;
+            if (o.status == 1) {
+                char buf[256];
+                snprintf(buf, sizeof buf, "preconditioner not SPD on subspace: r'z = %.3e at iteration %lld", o.value,
+                         (long long)o.at);
+                throw Status{VS_ERUNTIME, buf};
             }
         }
+        for (int64_t k = 0; k < cfg->max_iter && !c->h_ost->converged; ++k) {
+            outer_op(P_D, P_Q);
+            c->reduce_dev(1, 1, P_D, P_Q, Q_DQ);
+            launch_outer(SO_ALPHA, c->ost, c->scal, R, 0, k, 0, 0, c->hist, s);  // alpha = rz / d'q
+            ++c->launches;
+            c->vec(1, 1, -1, P_X, P_D, 0.0, alpha);    // x -= alpha d
+            c->vec(1, 1, -1, P_R, P_Q, 0.0, alpha);    // r -= alpha q
+            c->vec(0, 2, -1, U_ITER, U_W, 0.0, alpha);  // u += alpha w (schur.py:334-336)
+            perm(U_ITER, k);
+            outer_prec(P_R, P_Z);
+            norms();
+            launch_outer(SO_BETA, c->ost, c->scal, R, 0, k, cfg->eps_S, use_prec, c->hist, s);
+            ++c->launches;
+            c->vec(1, 3, P_D, P_D, P_Z, 0.0, beta);  // d = z + beta d (unused once converged)
+            settle(0);
+        }
+        const int64_t its = c->h_ost->its;
+        const bool conv = c->h_ost->converged != 0;
         // refresh: A u = f - B^T p, warm start from u (schur.py:352-357)
         c->grad(P_X, U_TMP);
         c->force(U_RHS, U_TMP);
-        tot_vel += cg_solve(c, 0, U_RHS, U_ITER, cfg->eps_A, U_ITER);
-        const double kval = perm(U_ITER);
-        ph.back() = kval;
+        cg_async(c, 0, U_RHS, U_ITER, cfg->eps_A, U_ITER);
+        c->reduce_dev(0, 0, U_ITER, -1, Q_PERM, c->flow_dir);
+        CK(cudaMemcpyAsync(c->h_scal, c->scal, Q_COUNT * R * sizeof(double), cudaMemcpyDeviceToHost, s));
+        settle(0);
+        double ksum = c->h_scal[Q_PERM * R];
+        for (int q = 1; q < R; ++q) ksum = ksum + c->h_scal[Q_PERM * R + q];
+        const double kval = cfg->h_pow_dim * ksum;
         CK(cudaEventRecord(c->ev1, s));
         c->download(1, P_X, pressure);
         c->download(0, U_ITER, velocity);
+        std::vector<double> h(5 * hs);
+        CK(cudaMemcpyAsync(h.data(), c->hist, 5 * hs * sizeof(double), cudaMemcpyDeviceToHost, s));
         c->sync();
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        h[4 * hs + its] = kval;  // perm_history[-1] = k of the refreshed velocity (schur.py:357)
         rep->k_value = kval;
         rep->iters_outer = its;
         rep->converged = conv ? 1 : 0;
         rep->inner_velocity = tot_vel;
         rep->inner_preconditioner = tot_pre;
-        rep->n_hist = (int64_t)ph.size();
+        rep->n_hist = its + 1;
         rep->device_ms = ms;
-        auto put = [](double *dst, const std::vector<double> &v) {
-            if (dst && !v.empty()) memcpy(dst, v.data(), v.size() * sizeof(double));
+        auto put = [&](double *dst, int which, int64_t cnt) {
+            if (dst && cnt > 0) memcpy(dst, h.data() + which * hs, cnt * sizeof(double));
         };
-        put(res_prec, rp);
-        put(res_unprec, ru);
-        put(perm_history, ph);
-        put(alpha_out, al);
-        put(beta_out, be);
+        put(alpha_out, 0, its);
+        put(beta_out, 1, its);
+        put(res_prec, 2, its + 1);
+        put(res_unprec, 3, its + 1);
+        put(perm_history, 4, its + 1);
     });
 }
 

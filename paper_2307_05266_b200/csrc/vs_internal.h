@@ -84,7 +84,19 @@ void launch_apply_S(const Geo &g, const uint64_t *prec, const double *p, double 
                     const double *invA_enc, double inv_h, cudaStream_t s);
 void launch_dwd(const Geo &g, const uint64_t *prec, const double *w, double *out, int64_t m, double inv_h2,
                 cudaStream_t s);
-void launch_vec(int kind, double *out, double *a, const double *b, double sc, int64_t m, cudaStream_t s);
+void launch_vec(int kind, double *out, double *a, const double *b, double sc, const double *sp, int64_t m,
+                cudaStream_t s);
+
+// device-side state of the outer PCG (vs_api.cu drives it, one sync per outer iteration)
+struct OuterState {
+    double rz, alpha, beta, mu, ref, value;
+    int32_t status, converged;  // status: 1 r'z < 0, 2 d'q <= 0, 3 non-finite
+    int64_t at, its, hstride;
+};
+enum { SO_MEAN, SO_PERM, SO_INIT, SO_ALPHA, SO_BETA };
+enum { Q_DQ, Q_PERM, Q_MU, Q_RZ, Q_ZZ, Q_RR, Q_COUNT };  // reduction slots (x R slabs)
+void launch_outer(int op, OuterState *st, const double *scal, int R, double arg, int64_t k, double eps,
+                  int use_prec, double *hist, cudaStream_t s);
 void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s);
 int launch_reduce(int kind, const double *a, const double *b, int64_t m, double *part, double *out,
                   cudaStream_t s);

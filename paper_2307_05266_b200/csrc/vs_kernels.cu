@@ -231,9 +231,11 @@ __global__ void k_dwd(Geo g, const uint64_t *prec, const double *w, double *out,
 // ------------------------------------------------------ outer vector ops
 
 // kind: 0 out=a-s ; 1 a-=s*b ; 2 a+=s*b ; 3 out=b+s*a (d = z + beta d) ; 4 out=a-b
-__global__ void k_vec(int kind, double *out, double *a, const double *b, double s, int64_t m) {
+// s comes from the device scalar *sp when sp != nullptr (outer loop state)
+__global__ void k_vec(int kind, double *out, double *a, const double *b, double s0, const double *sp, int64_t m) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= m) return;
+    const double s = sp ? *sp : s0;
     switch (kind) {
         case 0: out[i] = __dsub_rn(a[i], s); break;
         case 1: a[i] = __dsub_rn(a[i], __dmul_rn(s, b[i])); break;
@@ -345,8 +347,71 @@ void launch_dwd(const Geo &g, const uint64_t *prec, const double *w, double *out
                 cudaStream_t s) {
     if (m) k_dwd<<<nblk(m), 256, 0, s>>>(g, prec, w, out, m, inv_h2);
 }
-void launch_vec(int kind, double *out, double *a, const double *b, double sc, int64_t m, cudaStream_t s) {
-    if (m) k_vec<<<nblk(m), 256, 0, s>>>(kind, out, a, b, sc, m);
+void launch_vec(int kind, double *out, double *a, const double *b, double sc, const double *sp, int64_t m,
+                cudaStream_t s) {
+    if (m) k_vec<<<nblk(m), 256, 0, s>>>(kind, out, a, b, sc, sp, m);
+}
+
+// ---- device-side scalar steps of the outer PCG (krylov.py:102-182, schur.py:288)
+__device__ __forceinline__ double slab_sum(const double *scal, int q, int R) {
+    double t = scal[q * R];
+    for (int s = 1; s < R; ++s) t = t + scal[q * R + s];
+    return t;
+}
+
+__global__ void k_outer(int op, OuterState *st, const double *scal, int R, double arg, int64_t k, double eps,
+                        int use_prec, double *hist) {
+    // hist layout: [0] alpha, [1] beta, [2] res_prec, [3] res_unprec, [4] perm; stride HSTRIDE
+    double *h_alpha = hist, *h_beta = hist + st->hstride, *h_rp = hist + 2 * st->hstride,
+           *h_ru = hist + 3 * st->hstride, *h_perm = hist + 4 * st->hstride;
+    auto flag = [&](int code, double val, int64_t at) {
+        if (!st->status) { st->status = code; st->value = val; st->at = at; }
+    };
+    switch (op) {
+        case SO_MEAN: st->mu = slab_sum(scal, Q_MU, R) / arg; break;  // arg = m
+        case SO_PERM: h_perm[k + 1] = arg * slab_sum(scal, Q_PERM, R); break;  // arg = h**dim
+        case SO_INIT: {  // krylov.py:120-128
+            const double rp = sqrt(slab_sum(scal, Q_ZZ, R)), ru = sqrt(slab_sum(scal, Q_RR, R));
+            h_rp[0] = rp;
+            h_ru[0] = ru;
+            st->ref = use_prec ? rp : ru;
+            st->converged = st->ref == 0.0;
+            st->rz = slab_sum(scal, Q_RZ, R);
+            st->its = 0;
+            if (!st->converged) {
+                if (st->rz < 0.0) flag(1, st->rz, 0);
+                else if (st->rz == 0.0) st->converged = 1;
+            }
+            break;
+        }
+        case SO_ALPHA: {  // krylov.py:139-146
+            const double dq = slab_sum(scal, Q_DQ, R);
+            if (dq <= 0.0) flag(2, dq, k);
+            st->alpha = st->rz / dq;
+            h_alpha[k] = st->alpha;
+            break;
+        }
+        case SO_BETA: {  // krylov.py:154-169, then the next iteration's r'z checks (:131-137)
+            const double rz_new = slab_sum(scal, Q_RZ, R);
+            st->beta = rz_new / st->rz;
+            st->rz = rz_new;
+            const double nz = sqrt(slab_sum(scal, Q_ZZ, R)), nr = sqrt(slab_sum(scal, Q_RR, R));
+            if (!(isfinite(nz) && isfinite(nr))) { flag(3, 0.0, k + 1); break; }
+            h_beta[k] = st->beta;
+            h_rp[k + 1] = nz;
+            h_ru[k + 1] = nr;
+            st->its = k + 1;
+            if ((use_prec ? nz : nr) / st->ref < eps) { st->converged = 1; break; }
+            if (st->rz < 0.0) flag(1, st->rz, k + 1);
+            else if (st->rz == 0.0) st->converged = 1;
+            break;
+        }
+    }
+}
+
+void launch_outer(int op, OuterState *st, const double *scal, int R, double arg, int64_t k, double eps,
+                  int use_prec, double *hist, cudaStream_t s) {
+    k_outer<<<1, 1, 0, s>>>(op, st, scal, R, arg, k, eps, use_prec, hist);
 }
 void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s) {
     if (m) k_force<<<nblk(m), 256, 0, s>>>(out, sub, lo, cnt, m);
