@@ -18,6 +18,8 @@
 // DRAM bytes per DOF per iteration (8 B each): P1 reads z, d_old, record and
 // writes d; P2 reads d, x, r, record and writes x, r, z  -> 88 B (plus
 // L2-resident bitmask words for the neighbour ranks).
+#include <cstdlib>
+
 #include "vs_device.cuh"
 #include "vs_internal.h"
 
@@ -545,7 +547,8 @@ CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     const int ns = 2 * dim;
-    const size_t budget = std::min<size_t>(CG_SMEM_BUDGET, (size_t)maxopt);
+    size_t budget = std::min<size_t>(CG_SMEM_BUDGET, (size_t)maxopt);
+    if (const char *e = getenv("VOXSCHUR_SMEM_KB")) budget = std::min<size_t>(budget, (size_t)atoi(e) * 1024);
     for (int tier = 2; tier >= 1; --tier) {
         const void *fn = pcg_fn(dim, op, tier);
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
