@@ -99,6 +99,22 @@ int vs_ctx_create2(const uint8_t *fluid, int dim, int n, int flow_dir,
                    double inv_h, double inv_h2, int slabs, vs_ctx **out);
 int vs_slab_count(vs_ctx *ctx);
 
+/* Multi-GPU, one process per GPU: context for rank `rank` of `nranks`
+ * (slab decomposition as vs_ctx_create2 with slabs = nranks, but this process
+ * holds only its own slab, in one device arena).  Exchange the 64-byte
+ * vs_ipc_handle of every rank (e.g. torch.distributed all_gather_object),
+ * then vs_ipc_attach with all handles in rank order; afterwards every rank
+ * calls the same solves -- the fused kernels exchange ghost planes and
+ * reduction partials through peer-mapped NVLink memory and share rank 0's
+ * barrier counter.  Host vectors in/out carry only this rank's owned DOFs
+ * (in reference positions). */
+int vs_ctx_create_rank(const uint8_t *fluid, int dim, int n, int flow_dir,
+                       int check_connectivity, int require_walls, int device,
+                       double inv_h, double inv_h2, int rank, int nranks,
+                       vs_ctx **out);
+int vs_ipc_handle(vs_ctx *ctx, void *handle64);
+int vs_ipc_attach(vs_ctx *ctx, const void *handles);
+
 /* Host-only slab plan of a mask (no device needed): for each slab 42 int64 =
  * x_lo, x_hi; per family (velocity 0, 1, 2, pressure): own, own_off,
  * glo_off, glo_cnt, ghi_off, ghi_cnt, first_cnt, last_cnt, gstart; then

@@ -6,7 +6,7 @@ every apply and solve runs in libvoxschur.so (sm_100a CUDA).
 """
 from .geometry import VoxelGrid, connected_components, enforce_connectivity
 from .krylov import PcgConfig, PcgResult, jacobi_prec, lanczos_condition_estimate, pcg
-from .operators import DofMap, StaggeredSystem, assemble, axis_index
+from .operators import DofMap, StaggeredSystem, assemble, axis_index, connect_ranks
 from .schur import (
     TOLERANCE_PROFILES,
     SchurConfig,
@@ -25,7 +25,7 @@ __version__ = "0.1.0"
 __all__ = [
     "VoxelGrid", "connected_components", "enforce_connectivity",
     "PcgConfig", "PcgResult", "jacobi_prec", "lanczos_condition_estimate", "pcg",
-    "DofMap", "StaggeredSystem", "assemble", "axis_index",
+    "DofMap", "StaggeredSystem", "assemble", "axis_index", "connect_ranks",
     "TOLERANCE_PROFILES", "SchurConfig", "SolveReport", "apply_schur", "apply_simple_inverse",
     "last_kernel_stats", "permeability", "profile_config", "schur_rhs", "solve_schur",
     "__version__",

@@ -80,6 +80,10 @@ def _load():
                                      C.c_double, C.c_double, C.c_int, C.POINTER(P)]),
         "vs_slab_count": (C.c_int, [P]),
         "vs_slab_plan": (C.c_int, [u8, C.c_int, C.c_int, C.c_int, P]),
+        "vs_ctx_create_rank": (C.c_int, [u8, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(P)]),
+        "vs_ipc_handle": (C.c_int, [P, P]),
+        "vs_ipc_attach": (C.c_int, [P, P]),
         "vs_ctx_destroy": (None, [P]),
         "vs_counts": (C.c_int, [P, i64p, i64p, i64p]),
         "vs_export_geometry": (C.c_int, [P, P, P, P, P, P]),
@@ -104,7 +108,8 @@ def _load():
 
 lib = _load()
 EXPORTED = (
-    "vs_last_error", "vs_version", "vs_components", "vs_stamp_balls", "vs_ctx_create", "vs_ctx_create2", "vs_slab_count", "vs_slab_plan", "vs_ctx_destroy",
+    "vs_last_error", "vs_version", "vs_components", "vs_stamp_balls", "vs_ctx_create", "vs_ctx_create2", "vs_slab_count", "vs_slab_plan", "vs_ctx_create_rank", "vs_ipc_handle", "vs_ipc_attach",
+    "vs_ctx_destroy",
     "vs_counts", "vs_export_geometry", "vs_apply_laplacian", "vs_apply_divergence",
     "vs_apply_gradient", "vs_divergence_weighted_diagonal", "vs_apply_simple",
     "vs_solve_velocity", "vs_solve_simple", "vs_solve_schur", "vs_kernel_stats",

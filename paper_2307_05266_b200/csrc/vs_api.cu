@@ -146,36 +146,59 @@ struct vs_ctx {
         if (h_cglog) cudaFreeHost(h_cglog);
         if (h_ost) cudaFreeHost(h_ost);
         for (cudaEvent_t e : evpool) cudaEventDestroy(e);
+        for (void *p : peer_arena)
+            if (p) cudaIpcCloseMemHandle(p);
         for (cudaEvent_t e : {ev0, ev1, evs0, evs1})
             if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
     }
     void sync() { CK(cudaStreamSynchronize(stream)); }
     int nfam() const { return dim; }
-    // ---- distributed-vector helpers (loop over slabs, fixed order)
-    double *U(int s, int slot) { return slabs[s].u[slot]; }
-    double *Pv(int s, int slot) { return slabs[s].p[slot]; }
+    // ---- slab-distributed helpers.  Slabs [s0, s1) are local (all of them
+    // in one process, or this rank's one on a multi-process run); remote
+    // slabs' vectors are peer-mapped pointers.  Loops run in slab order.
+    int s0 = 0, s1 = 1;                 // local slabs
+    int rank = 0, nranks = 1;           // process-level decomposition (nranks > 1: one slab per process)
+    double *scal_peer[VS_MAX_SLABS] = {};  // every rank's reduction slots
+    double *part_peer[VS_MAX_SLABS] = {};  // every rank's CG partial buffer
+    unsigned *bar_base = nullptr;       // local: value of the barrier counter after the last launch
+    char *arena = nullptr;              // this process's first local slab arena (IPC-exported)
+    void *peer_arena[VS_MAX_SLABS] = {};  // opened IPC mappings (closed on destroy)
+    int64_t tb_max = 0;
+    int npart = 1;
+    bool mp() const { return nranks > 1; }
+    // cross-rank device barrier (one arrival per rank; same counter as the CG)
+    void xbar() {
+        if (!mp()) return;
+        launch_xbar(bar, bar_base, nranks, stream);
+        ++launches;
+    }
+    // make this rank's reduction slots [q0, q1) visible in every rank's scal
+    void publish(int q0, int q1) {
+        if (!mp()) return;
+        for (int r = 0; r < nranks; ++r) {
+            if (r == rank) continue;
+            for (int q = q0; q < q1; ++q)
+                CK(cudaMemcpyAsync(scal_peer[r] + q * R + rank, scal + q * R + rank, sizeof(double),
+                                   cudaMemcpyDeviceToDevice, stream));
+        }
+        xbar();
+    }
     // deterministic reduction over the owned DOFs of every slab, result on host
     double reduce(int space, int kind, int a, int b, int64_t lo_fam = -1) {
-        double tot = 0.0;
-        for (int s = 0; s < R; ++s) {
-            Slab &S = slabs[s];
-            const double *pa = space == 0 ? S.u[a] : S.p[a];
-            const double *pb = b < 0 ? nullptr : (space == 0 ? S.u[b] : S.p[b]);
-            int64_t off = 0, m = S.m_own[space];
-            if (lo_fam >= 0) { off = S.own_off[lo_fam]; m = S.own[lo_fam]; }
-            launches += launch_reduce(kind, pa + off, pb ? pb + off : nullptr, m, red_part, scal + s, stream);
-        }
-        CK(cudaMemcpyAsync(h_scal, scal, R * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        reduce_dev(space, kind, a, b, Q_HOST, lo_fam);
+        publish(Q_HOST, Q_HOST + 1);
+        CK(cudaMemcpyAsync(h_scal, scal + Q_HOST * R, R * sizeof(double), cudaMemcpyDeviceToHost, stream));
         sync();
-        for (int s = 0; s < R; ++s) tot = (s == 0) ? h_scal[0] : tot + h_scal[s];
+        double tot = h_scal[0];
+        for (int s = 1; s < R; ++s) tot = tot + h_scal[s];
         return tot;
     }
     double dot(int space, int a, int b) { return reduce(space, 1, a, b); }
     double sum(int space, int a) { return reduce(space, 0, a, -1); }
     double mean(int space, int a) { return sum(space, a) / (double)(space == 0 ? m_u : m_p); }
     void vec(int space, int kind, int out, int a, int b, double sc, const double *sp = nullptr) {
-        for (int s = 0; s < R; ++s) {
+        for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
             double **v = space == 0 ? S.u : S.p;
             launch_vec(kind, out < 0 ? nullptr : v[out], v[a], b < 0 ? nullptr : v[b], sc, sp, S.m_own[space],
@@ -184,8 +207,9 @@ struct vs_ctx {
         }
     }
     // device-resident reduction into slot q (scal[q*R + s]); no host sync
+    // (callers publish() before a k_outer step reads the slots of all slabs)
     void reduce_dev(int space, int kind, int a, int b, int q, int64_t lo_fam = -1) {
-        for (int s = 0; s < R; ++s) {
+        for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
             const double *pa = space == 0 ? S.u[a] : S.p[a];
             const double *pb = b < 0 ? nullptr : (space == 0 ? S.u[b] : S.p[b]);
@@ -195,7 +219,7 @@ struct vs_ctx {
         }
     }
     void copy(int space, int dst, int src) {
-        for (int s = 0; s < R; ++s) {
+        for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
             double **v = space == 0 ? S.u : S.p;
             if (S.m_own[space])
@@ -203,30 +227,32 @@ struct vs_ctx {
                                    stream));
         }
     }
-    // fill the ghost planes of a vector from the neighbouring slabs' owned
-    // boundary planes (device-to-device; peer copies on a multi-GPU run)
+    // push every local slab's boundary planes into the neighbours' ghost
+    // planes (first owned plane -> lower slab's ghost_hi, last -> upper's
+    // ghost_lo); peer stores over NVLink on a multi-process run
     void halo(int space, int slot) {
         if (R == 1) return;
-        for (int s = 0; s < R; ++s) {
+        for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s], &lo = slabs[(s - 1 + R) % R], &hi = slabs[(s + 1) % R];
             const int nf = space == 0 ? dim : 1;
+            const double *src = space == 0 ? S.u[slot] : S.p[slot];
+            double *dlo = space == 0 ? lo.u[slot] : lo.p[slot];
+            double *dhi = space == 0 ? hi.u[slot] : hi.p[slot];
             for (int k = 0; k < nf; ++k) {
                 const int f = space == 0 ? k : FP;
-                double *dst = space == 0 ? S.u[slot] : S.p[slot];
-                const double *slo = space == 0 ? lo.u[slot] : lo.p[slot];
-                const double *shi = space == 0 ? hi.u[slot] : hi.p[slot];
-                if (S.glo_cnt[f])
-                    CK(cudaMemcpyAsync(dst + S.glo_off[f], slo + lo.own_off[f] + lo.own[f] - lo.last_cnt[f],
-                                       S.glo_cnt[f] * sizeof(double), cudaMemcpyDeviceToDevice, stream));
-                if (S.ghi_cnt[f])
-                    CK(cudaMemcpyAsync(dst + S.ghi_off[f], shi + hi.own_off[f], S.ghi_cnt[f] * sizeof(double),
+                if (S.first_cnt[f])
+                    CK(cudaMemcpyAsync(dlo + lo.ghi_off[f], src + S.own_off[f], S.first_cnt[f] * sizeof(double),
                                        cudaMemcpyDeviceToDevice, stream));
+                if (S.last_cnt[f])
+                    CK(cudaMemcpyAsync(dhi + hi.glo_off[f], src + S.own_off[f] + S.own[f] - S.last_cnt[f],
+                                       S.last_cnt[f] * sizeof(double), cudaMemcpyDeviceToDevice, stream));
             }
         }
+        xbar();  // every rank's pushes land before anyone reads its ghosts
     }
-    // host (reference order) -> slabs, owned and ghost planes
+    // host (reference order) -> local slabs, owned and ghost planes
     void upload(int space, int slot, const double *h) {
-        for (int s = 0; s < R; ++s) {
+        for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
             double *dst = space == 0 ? S.u[slot] : S.p[slot];
             const int nf = space == 0 ? dim : 1;
@@ -244,9 +270,10 @@ struct vs_ctx {
             }
         }
     }
+    // local slabs' owned DOFs -> host vector (reference order)
     void download(int space, int slot, double *h) {
         if (!h) return;
-        for (int s = 0; s < R; ++s) {
+        for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
             const double *src = space == 0 ? S.u[slot] : S.p[slot];
             const int nf = space == 0 ? dim : 1;
@@ -258,10 +285,10 @@ struct vs_ctx {
             }
         }
     }
-    // ---- outer operators on every slab (ghosts of the input refreshed first)
+    // ---- outer operators on every local slab (ghosts of the input refreshed first)
     void grad(int p_in, int u_out) {  // B^T: needs p at I - e_a
         halo(1, p_in);
-        for (int s = 0; s < R; ++s) {
+        for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
             launch_apply_grad(S.geo, S.vrec, S.p[p_in], S.u[u_out], S.m_own[0], inv_h, stream);
             ++launches;
@@ -269,14 +296,14 @@ struct vs_ctx {
     }
     void div(int u_in, int p_out) {  // B: needs u at I + e_a
         halo(0, u_in);
-        for (int s = 0; s < R; ++s) {
+        for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
             launch_apply_div(S.geo, S.prec, S.u[u_in], S.p[p_out], S.m_own[1], inv_h, stream);
             ++launches;
         }
     }
     void force(int out, int sub) {  // out = force (- sub)
-        for (int s = 0; s < R; ++s) {
+        for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
             launch_force(S.u[out], sub < 0 ? nullptr : S.u[sub], S.own_off[flow_dir], S.own[flow_dir], S.m_own[0],
                          stream);
@@ -384,10 +411,11 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     }
     if (x0 >= 0) c->halo(op == 0 ? 0 : 1, x0);  // A x0 needs x0 on the ghost planes
     const int ring = li % GROUP_RING;
-    CgGroup *hg = c->h_groups + ring * R;
-    for (int s = 0; s < R; ++s) {
+    const int nloc = c->s1 - c->s0;
+    CgGroup *hg = c->h_groups + ring * nloc;
+    for (int s = c->s0; s < c->s1; ++s) {
         Slab &S = c->slabs[s];
-        CgGroup &G = hg[s];
+        CgGroup &G = hg[s - c->s0];
         memset(&G, 0, sizeof G);
         double **v = op == 0 ? S.u : S.p;
         if (op == 0) {
@@ -422,17 +450,20 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
             }
         }
     }
-    CgGroup *dg = c->d_groups + ring * R;
-    CK(cudaMemcpyAsync(dg, hg, R * sizeof(CgGroup), cudaMemcpyHostToDevice, c->stream));
+    CgGroup *dg = c->d_groups + ring * nloc;
+    CK(cudaMemcpyAsync(dg, hg, nloc * sizeof(CgGroup), cudaMemcpyHostToDevice, c->stream));
     CgParams P;
     memset(&P, 0, sizeof P);
     P.groups = dg;
-    P.group_base = 0;
+    P.group_base = 0;  // groups[] holds this process's slabs only
     P.n = c->n;
     P.nw = c->nw;
     P.m_global = (double)m;
     P.part = c->part;
     P.bar = c->bar;
+    P.bar_base = c->bar_base;
+    P.npart = c->npart;
+    for (int r = 0; r < c->npart; ++r) P.part_peer[r] = c->part_peer[r];
     P.phase_ns = c->phase_ns;
     P.out = c->cglog + li;
     P.tol = eps;
@@ -446,15 +477,15 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.invS = c->invS;
     P.pf_dist = c->pf_dist;
     const CgPlan &pl = op == 0 ? c->plan_A : c->plan_S;
-    CK(cudaMemsetAsync(c->bar, 0, sizeof(unsigned), c->stream));
-    ++c->launches;
+    P.total_blocks = pl.grid * R;          // blocks of every rank
+    P.block_base = pl.grid * c->s0;        // global index of this launch's block 0
     while ((int)c->evpool.size() < 2 * c->ncglog) {
         cudaEvent_t e;
         CK(cudaEventCreate(&e));
         c->evpool.push_back(e);
     }
     CK(cudaEventRecord(c->evpool[2 * li], c->stream));
-    CK(launch_pcg(c->dim, op, pl, R, P, c->stream));
+    CK(launch_pcg(c->dim, op, pl, nloc, P, c->stream));
     CK(cudaEventRecord(c->evpool[2 * li + 1], c->stream));
     ++c->launches;
     return li;
@@ -576,8 +607,38 @@ void plan_slabs(const std::vector<int64_t> (&pstart)[4], int n, int dim, int R, 
     }
 }
 
-// Build the slabs of the decomposition from the global geometry.
-void build_slabs(vs_ctx *C, int R) {
+// Device arena of one slab: every vector slot, the CG partial buffer, the
+// reduction slots and the barrier words in ONE allocation, laid out by a
+// formula every rank can evaluate for every slab -- so a single CUDA IPC
+// handle per rank maps a neighbour's whole slab (vs_ipc_attach).
+struct ArenaLayout {
+    size_t u[NU], p[NP], part, scal, bar, bytes;
+};
+ArenaLayout arena_layout(const Slab &S, int64_t tb_max, int R) {
+    ArenaLayout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) / 256 * 256;
+        return o;
+    };
+    for (int k = 0; k < NU; ++k) L.u[k] = take(std::max<int64_t>(1, S.m_all[0]) * sizeof(double));
+    for (int k = 0; k < NP; ++k) L.p[k] = take(std::max<int64_t>(1, S.m_all[1]) * sizeof(double));
+    L.part = take((size_t)4 * 8 * tb_max * sizeof(double));
+    L.scal = take((size_t)Q_COUNT * R * sizeof(double));
+    L.bar = take(4 * sizeof(unsigned));
+    L.bytes = off;
+    return L;
+}
+
+void bind_arena(Slab &S, char *base, const ArenaLayout &L) {
+    for (int k = 0; k < NU; ++k) S.u[k] = (double *)(base + L.u[k]);
+    for (int k = 0; k < NP; ++k) S.p[k] = (double *)(base + L.p[k]);
+}
+
+// Build the decomposition from the global geometry: R slabs in total, of
+// which this process holds [s0, s1) (all of them, or `rank`'s one).
+void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
     const int n = C->n, dim = C->dim;
     const int64_t wpp = (int64_t)(dim == 3 ? n : 1) * C->nw;  // meta words per x-plane
     // plane starts per family, from the first word of each plane
@@ -593,8 +654,23 @@ void build_slabs(vs_ctx *C, int R) {
         C->pstart[f][n] = f == FP ? C->m_p : C->voff[f] + C->vcount[f];
     }
     C->R = R;
+    C->rank = rank;
+    C->nranks = nranks;
+    C->s0 = nranks > 1 ? rank : 0;
+    C->s1 = nranks > 1 ? rank + 1 : R;
+    const int nloc = C->s1 - C->s0;
     plan_slabs(C->pstart, n, dim, R, C->slabs);
-    for (int s = 0; s < R; ++s) {
+    // plans from the largest slab of the whole decomposition, so every rank
+    // launches the same grid (the barrier counts all ranks' blocks)
+    int64_t mu_max = 0, mp_max = 0;
+    for (auto &S : C->slabs) {
+        mu_max = std::max(mu_max, S.m_own[0]);
+        mp_max = std::max(mp_max, S.m_own[1]);
+    }
+    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device);
+    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device);
+    C->tb_max = (int64_t)std::max(C->plan_A.grid, C->plan_S.grid) * R;
+    for (int s = C->s0; s < C->s1; ++s) {
         Slab &S = C->slabs[s];
         // geometry
         if (R == 1) {
@@ -627,20 +703,23 @@ void build_slabs(vs_ctx *C, int R) {
         S.geo.fbits = nullptr;
         for (int a = 0; a < 3; ++a) S.geo.vmeta[a] = S.meta[a];
         S.geo.pmeta = S.meta[FP];
-        for (int k = 0; k < NU; ++k) S.u[k] = C->alloc<double>(S.m_all[0]);
-        for (int k = 0; k < NP; ++k) S.p[k] = C->alloc<double>(S.m_all[1]);
+        const ArenaLayout L = arena_layout(S, C->tb_max, R);
+        char *base = C->alloc<char>(L.bytes);
+        bind_arena(S, base, L);
+        if (s == C->s0) {
+            C->arena = base;
+            C->part = (double *)(base + L.part);
+            C->scal = (double *)(base + L.scal);
+            C->bar = (unsigned *)(base + L.bar);  // rank 0's counter replaces it on attach
+            C->bar_base = C->bar + 1;
+            CK(cudaMemsetAsync(C->bar, 0, 4 * sizeof(unsigned), C->stream));
+        }
     }
-    int64_t mu_max = 0, mp_max = 0;
-    for (auto &S : C->slabs) {
-        mu_max = std::max(mu_max, S.m_own[0]);
-        mp_max = std::max(mp_max, S.m_own[1]);
-    }
-    C->plan_A = pcg_plan(dim, 0, mu_max, R, C->device);
-    C->plan_S = pcg_plan(dim, 1, mp_max, R, C->device);
-    C->part = C->alloc<double>((size_t)4 * 8 * R * std::max(C->plan_A.grid, C->plan_S.grid));
-    C->d_groups = C->alloc<CgGroup>(R * GROUP_RING);
-    CK(cudaMallocHost(&C->h_groups, R * GROUP_RING * sizeof(CgGroup)));
-    C->scal = C->alloc<double>(std::max(8, Q_COUNT * R));
+    C->npart = 1;
+    C->part_peer[0] = C->part;
+    C->scal_peer[C->rank] = C->scal;
+    C->d_groups = C->alloc<CgGroup>(nloc * GROUP_RING);
+    CK(cudaMallocHost(&C->h_groups, nloc * GROUP_RING * sizeof(CgGroup)));
     CK(cudaFreeHost(C->h_scal));
     CK(cudaMallocHost(&C->h_scal, std::max(8, Q_COUNT * R) * sizeof(double)));
     C->cglog_cap = 16;
@@ -761,8 +840,9 @@ int vs_slab_plan(const uint8_t *fluid, int dim, int n, int slabs, int64_t *out) 
     return VS_OK;
 }
 
-int vs_ctx_create2(const uint8_t *fluid, int dim, int n, int flow_dir, int check_connectivity, int require_walls,
-                   int device, double inv_h, double inv_h2, int slabs, vs_ctx **out) {
+static int create_common(const uint8_t *fluid, int dim, int n, int flow_dir, int check_connectivity,
+                         int require_walls, int device, double inv_h, double inv_h2, int slabs, int rank,
+                         int nranks, vs_ctx **out) {
     *out = nullptr;
     if (dim != 2 && dim != 3) return fail(VS_EVALUE, "grid dimension must be 2 or 3, got %d", dim);
     if (n < 2) return fail(VS_EVALUE, "grid extent must be at least 2, got %d", n);
@@ -887,9 +967,7 @@ int vs_ctx_create2(const uint8_t *fluid, int dim, int n, int flow_dir, int check
         C->sync();
         C->sdiag_ok = hflag == 0;
         // ---- decomposition into x-slabs (1 = whole domain), work vectors, plans
-        build_slabs(C, slabs);
-        C->bar = C->alloc<unsigned>(2);
-        CK(cudaMemsetAsync(C->bar, 0, 2 * sizeof(unsigned), C->stream));
+        build_slabs(C, slabs, rank, nranks);
         if (const char *pf = getenv("VOXSCHUR_PREFETCH")) C->pf_dist = (uint32_t)atoi(pf);
         if (getenv("VOXSCHUR_PHASE_TIMING")) {
             C->phase_ns = C->alloc<unsigned long long>(12);
@@ -904,9 +982,64 @@ int vs_ctx_create2(const uint8_t *fluid, int dim, int n, int flow_dir, int check
     return VS_OK;
 }
 
+int vs_ctx_create2(const uint8_t *fluid, int dim, int n, int flow_dir, int check_connectivity, int require_walls,
+                   int device, double inv_h, double inv_h2, int slabs, vs_ctx **out) {
+    return create_common(fluid, dim, n, flow_dir, check_connectivity, require_walls, device, inv_h, inv_h2, slabs, 0,
+                         1, out);
+}
+
 int vs_ctx_create(const uint8_t *fluid, int dim, int n, int flow_dir, int check_connectivity, int require_walls,
                   int device, double inv_h, double inv_h2, vs_ctx **out) {
-    return vs_ctx_create2(fluid, dim, n, flow_dir, check_connectivity, require_walls, device, inv_h, inv_h2, 1, out);
+    return create_common(fluid, dim, n, flow_dir, check_connectivity, require_walls, device, inv_h, inv_h2, 1, 0, 1,
+                         out);
+}
+
+int vs_ctx_create_rank(const uint8_t *fluid, int dim, int n, int flow_dir, int check_connectivity,
+                       int require_walls, int device, double inv_h, double inv_h2, int rank, int nranks,
+                       vs_ctx **out) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(VS_EVALUE, "rank %d out of range for %d ranks", rank, nranks);
+    return create_common(fluid, dim, n, flow_dir, check_connectivity, require_walls, device, inv_h, inv_h2, nranks,
+                         rank, nranks, out);
+}
+
+// CUDA IPC: the local slab's arena handle (64 bytes) for the other ranks
+int vs_ipc_handle(vs_ctx *c, void *handle64) {
+    return guarded(c, [&] {
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, c->arena));
+        memcpy(handle64, &h, sizeof h);
+    });
+}
+
+// CUDA IPC: map every other rank's slab arena (handles: nranks x 64 bytes in
+// rank order), bind the remote slabs' vectors, CG partial buffers and
+// reduction slots to peer pointers, and use rank 0's barrier counter.
+int vs_ipc_attach(vs_ctx *c, const void *handles) {
+    return guarded(c, [&] {
+        if (!c->mp()) throw Status{VS_EVALUE, "vs_ipc_attach needs a context from vs_ctx_create_rank with nranks > 1"};
+        const int R = c->R;
+        for (int r = 0; r < R; ++r) {
+            Slab &S = c->slabs[r];
+            const ArenaLayout L = arena_layout(S, c->tb_max, R);
+            char *base = nullptr;
+            if (r == c->rank) {
+                base = c->arena;
+            } else {
+                cudaIpcMemHandle_t h;
+                memcpy(&h, (const char *)handles + (size_t)r * sizeof h, sizeof h);
+                void *p = nullptr;
+                CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+                c->peer_arena[r] = p;
+                base = (char *)p;
+                bind_arena(S, base, L);
+            }
+            c->part_peer[r] = (double *)(base + L.part);
+            c->scal_peer[r] = (double *)(base + L.scal);
+            if (r == 0) c->bar = (unsigned *)(base + L.bar);  // the shared counter lives on rank 0
+        }
+        c->npart = R;
+        c->sync();
+    });
 }
 
 void vs_ctx_destroy(vs_ctx *ctx) { delete ctx; }
@@ -945,7 +1078,7 @@ static int apply_common(vs_ctx *c, int which, const double *in, double *out) {
         const bool in_u = (which == 0 || which == 1 || which == 3);
         const bool out_u = (which == 0 || which == 2);
         c->upload(in_u ? 0 : 1, in_u ? U_IN : P_IN, in);  // owned + ghost planes from the host vector
-        for (int s = 0; s < c->R; ++s) {
+        for (int s = c->s0; s < c->s1; ++s) {
             Slab &S = c->slabs[s];
             const double *din = in_u ? S.u[U_IN] : S.p[P_IN];
             double *dout = out_u ? S.u[U_TMP] : S.p[P_TMP];
@@ -1022,11 +1155,13 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
         CK(cudaEventRecord(c->ev0, s));
         auto perm = [&](int slot, int64_t k) {  // schur.py:288 -> hist perm[k + 1]
             c->reduce_dev(0, 0, slot, -1, Q_PERM, c->flow_dir);
+            c->publish(Q_PERM, Q_PERM + 1);
             launch_outer(SO_PERM, c->ost, c->scal, R, cfg->h_pow_dim, k, 0, 0, c->hist, s);
             ++c->launches;
         };
         auto mean_into_mu = [&](int slot) {
             c->reduce_dev(1, 0, slot, -1, Q_MU);
+            c->publish(Q_MU, Q_MU + 1);
             launch_outer(SO_MEAN, c->ost, c->scal, R, (double)c->m_p, 0, 0, 0, c->hist, s);
             ++c->launches;
         };
@@ -1098,6 +1233,7 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
             c->reduce_dev(1, 1, P_R, P_Z, Q_RZ);
             c->reduce_dev(1, 1, P_Z, P_Z, Q_ZZ);
             c->reduce_dev(1, 1, P_R, P_R, Q_RR);
+            c->publish(Q_RZ, Q_RR + 1);
         };
         // u = u_f.copy(); perm_history = [k(u)]
         c->copy(0, U_ITER, U_F);
@@ -1105,7 +1241,8 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
         // ---- outer pcg setup with project_nullspace=True (krylov.py:102-128)
         mean_into_mu(P_B);
         c->vec(1, 0, P_B, P_B, -1, 0.0, mu);  // rhs -= mean(rhs)
-        for (auto &S : c->slabs) CK(cudaMemsetAsync(S.p[P_X], 0, S.m_all[1] * sizeof(double), s));  // x = 0
+        for (int q = c->s0; q < c->s1; ++q)  // x = 0
+            CK(cudaMemsetAsync(c->slabs[q].p[P_X], 0, c->slabs[q].m_all[1] * sizeof(double), s));
         outer_op(P_X, P_Q);
         c->vec(1, 4, P_R, P_Q, P_B, 0.0);  // r = op(x) - rhs
         outer_prec(P_R, P_Z);
@@ -1137,6 +1274,7 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
         for (int64_t k = 0; k < cfg->max_iter && !c->h_ost->converged; ++k) {
             outer_op(P_D, P_Q);
             c->reduce_dev(1, 1, P_D, P_Q, Q_DQ);
+            c->publish(Q_DQ, Q_DQ + 1);
             launch_outer(SO_ALPHA, c->ost, c->scal, R, 0, k, 0, 0, c->hist, s);  // alpha = rz / d'q
             ++c->launches;
             c->vec(1, 1, -1, P_X, P_D, 0.0, alpha);    // x -= alpha d
@@ -1157,6 +1295,7 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
         c->force(U_RHS, U_TMP);
         cg_async(c, 0, U_RHS, U_ITER, cfg->eps_A, U_ITER);
         c->reduce_dev(0, 0, U_ITER, -1, Q_PERM, c->flow_dir);
+        c->publish(Q_PERM, Q_PERM + 1);
         CK(cudaMemcpyAsync(c->h_scal, c->scal, Q_COUNT * R * sizeof(double), cudaMemcpyDeviceToHost, s));
         settle(0);
         double ksum = c->h_scal[Q_PERM * R];

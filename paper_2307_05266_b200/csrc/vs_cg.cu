@@ -154,17 +154,20 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// bar[0] = monotonic arrival counter, zeroed by the host before each launch.
-// Barrier number b (1-based) completes when the counter reaches b*gridDim.x:
-// one red.release per block, then thread 0 polls with acquire loads.
+// bar = monotonic arrival counter shared by every block of every rank; it is
+// never reset.  Each launch starts from *P.bar_base (the previous launch's
+// final target, written back by its block 0 -- identical on every rank, since
+// all ranks run the same barrier sequence) and each barrier adds the number
+// of participating blocks of all ranks.  One red.release per block, then
+// thread 0 polls.
 // (Measured on B200: ~1.2-1.4 us per barrier for 148-296 blocks, the same
 // as cooperative_groups grid.sync; tools/gridsync_micro.cu.)
 // Polling uses relaxed loads: an acquire load per poll makes ptxas emit an
 // L1 invalidation (CCTL.IVALL) per poll, which wipes the L1 of the other
 // block still computing on the same SM.  One acquire fence after the poll.
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target) {
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, unsigned total_blocks) {
     __syncthreads();
-    target += gridDim.x;
+    target += total_blocks;
     if (threadIdx.x == 0) {
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
         while ((int)(ld_relaxed(bar) - target) < 0) {
@@ -199,15 +202,18 @@ __device__ __forceinline__ void warp_tree(double (&t)[K]) {
     }
 }
 
-// Deterministic grid-wide sum of K values.  Each block writes its K block
-// sums block-major (part[b*8 + k]); after the barrier every block reads ALL
-// block sums in one parallel round trip (thread t <- block t) and reduces
-// them in the same fixed tree, so every block obtains bitwise-identical
-// totals (no serial chain of dependent L2 loads).
+// Deterministic grid-wide sum of K values over every block of every rank.
+// Block g (global index block_base + blockIdx.x) writes its K sums into slot
+// g of partial set `set` of EVERY rank's partial buffer (peer stores on a
+// multi-GPU run; one buffer when the ranks are groups of one launch).  After
+// the barrier each block reads all blocks' sums from its own buffer in one
+// parallel round trip and reduces them in the same fixed tree, so every
+// block of every rank obtains bitwise-identical totals.
 template <int K>
-__device__ __forceinline__ void grid_sum(double (&v)[K], double *part, unsigned *bar, unsigned &target,
+__device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams &P, unsigned &target,
                                          double (*s_warp)[5], double *s_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int TB = P.total_blocks;
     warp_tree<K>(v);
     if (lane == 0) {
 #pragma unroll
@@ -217,16 +223,19 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], double *part, unsigned 
     if (warp == 0) {
         double t[K];
         warp0_combine<K>(s_warp, t);
-        if (lane == 0) {
+        if (lane < P.npart) {  // lane p stores to rank p's buffer
+            double *dst = P.part_peer[lane] + (size_t)set * 8 * TB + (size_t)(P.block_base + blockIdx.x) * 8;
+            __builtin_assume(__isGlobal(dst));
 #pragma unroll
-            for (int k = 0; k < K; ++k) part[blockIdx.x * 8 + k] = t[k];
+            for (int k = 0; k < K; ++k) dst[k] = t[k];
         }
     }
-    grid_barrier(bar, target);  // starts with __syncthreads (s_warp reuse is safe)
+    grid_barrier(P.bar, target, TB);  // starts with __syncthreads (s_warp reuse is safe)
+    const double *part = P.part + (size_t)set * 8 * TB;
     double t[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) t[k] = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += CG_THREADS) {
+    for (int b = threadIdx.x; b < TB; b += CG_THREADS) {
 #pragma unroll
         for (int k = 0; k < K; ++k) t[k] = __dadd_rn(t[k], __ldcg(part + b * 8 + k));
     }
@@ -307,7 +316,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
         s_tab[16 + threadIdx.x] = P.inv_code[threadIdx.x];
         if (threadIdx.x < 8) s_tab[32 + threadIdx.x] = P.invA_enc[threadIdx.x];
     }
-    unsigned gen = 0;  // barrier target (counter zeroed by the host)
+    unsigned gen = __ldcg(P.bar_base);  // barrier target: where the previous launch left the counter
     const uint32_t kc = P.cache_slots;
     DofCache<DIM, OP, TIER> cache(dyn_smem, kc);
     __syncthreads();
@@ -332,7 +341,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
     if (PROJ) {
         double v[1] = {0.0};
         for (uint32_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], G.rhs[i]);
-        grid_sum<1>(v, P.part, P.bar, gen, s_warp, s_tot);
+        grid_sum<1>(v, 0, P, gen, s_warp, s_tot);
         mu_rhs = v[0] / P.m_global;
     }
     {
@@ -368,7 +377,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
             v[3] = __dadd_rn(v[3], zi);
             v[4] = __dadd_rn(v[4], ri);
         }
-        grid_sum<5>(v, P.part + 8 * gridDim.x, P.bar, gen, s_warp, s_tot);
+        grid_sum<5>(v, 1, P, gen, s_warp, s_tot);
         if (PROJ) {
             mu = v[3] / P.m_global;
             v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
@@ -436,7 +445,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                 dnew[i] = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dold[i]));
             }
             const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            grid_sum<1>(v1, P.part + 16 * gridDim.x, P.bar, gen, s_warp, s_tot);
+            grid_sum<1>(v1, 2, P, gen, s_warp, s_tot);
             const uint64_t t2 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             const double dq = v1[0];
             if (dq <= 0.0) { status = 2; sval = dq; sat = it; break; }
@@ -484,7 +493,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                 }
             }
             const uint64_t t3 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            grid_sum<KL>(v, P.part + 24 * gridDim.x, P.bar, gen, s_warp, s_tot);
+            grid_sum<KL>(v, 3, P, gen, s_warp, s_tot);
             if (P.phase_ns && threadIdx.x == 0) {
                 const uint64_t t4 = gtimer();
                 ph[0] += t1 - t0;
@@ -517,6 +526,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *P.bar_base = gen;  // the next launch on this stream starts from here
         CgOut *o = P.out;
         o->iterations = its;
         o->converged = conv ? 1 : 0;

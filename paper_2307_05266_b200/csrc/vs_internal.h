@@ -43,8 +43,13 @@ struct CgParams {
     int group_base, bpg;    // group of block b = group_base + b / bpg
     int n, nw;
     double m_global;        // DOFs summed over groups (for the mean projection)
-    double *part;           // 4 sets x 8 slots x (all blocks)
-    unsigned *bar;          // grid barrier counter
+    double *part;           // this rank's partial buffer: 4 sets x 8 slots x total_blocks
+    unsigned *bar;          // grid barrier counter (rank 0's on a multi-GPU run)
+    unsigned *bar_base;     // local: counter value reached by the previous launch
+    int total_blocks;       // blocks of all ranks in this solve
+    int block_base;         // global index of this launch's block 0
+    int npart;              // ranks whose partial buffers receive this launch's sums
+    double *part_peer[VS_MAX_SLABS];
     CgOut *out;
     double tol;
     int64_t max_iter;
@@ -94,7 +99,8 @@ struct OuterState {
     int64_t at, its, hstride;
 };
 enum { SO_MEAN, SO_PERM, SO_INIT, SO_ALPHA, SO_BETA };
-enum { Q_DQ, Q_PERM, Q_MU, Q_RZ, Q_ZZ, Q_RR, Q_COUNT };  // reduction slots (x R slabs)
+enum { Q_DQ, Q_PERM, Q_MU, Q_RZ, Q_ZZ, Q_RR, Q_HOST, Q_COUNT };  // reduction slots (x R slabs)
+void launch_xbar(unsigned *bar, unsigned *bar_base, int nranks, cudaStream_t s);
 void launch_outer(int op, OuterState *st, const double *scal, int R, double arg, int64_t k, double eps,
                   int use_prec, double *hist, cudaStream_t s);
 void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s);

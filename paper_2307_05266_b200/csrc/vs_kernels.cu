@@ -409,6 +409,22 @@ __global__ void k_outer(int op, OuterState *st, const double *scal, int R, doubl
     }
 }
 
+// cross-rank barrier for the outer loop: one arrival per rank on the
+// counter the fused CG uses (its base carried in *bar_base)
+__global__ void k_xbar(unsigned *bar, unsigned *bar_base, int nranks) {
+    const unsigned target = *bar_base + (unsigned)nranks;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while ((int)(v - target) < 0);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    *bar_base = target;
+}
+void launch_xbar(unsigned *bar, unsigned *bar_base, int nranks, cudaStream_t s) {
+    k_xbar<<<1, 1, 0, s>>>(bar, bar_base, nranks);
+}
+
 void launch_outer(int op, OuterState *st, const double *scal, int R, double arg, int64_t k, double eps,
                   int use_prec, double *hist, cudaStream_t s) {
     k_outer<<<1, 1, 0, s>>>(op, st, scal, R, arg, k, eps, use_prec, hist);

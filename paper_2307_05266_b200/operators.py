@@ -19,7 +19,7 @@ import numpy as np
 from . import _lib
 from .geometry import VoxelGrid
 
-__all__ = ["DofMap", "StaggeredSystem", "assemble", "axis_index"]
+__all__ = ["DofMap", "StaggeredSystem", "assemble", "axis_index", "connect_ranks"]
 
 _AXIS_NAMES = {"x": 0, "y": 1, "z": 2}
 
@@ -179,14 +179,16 @@ def _default_device() -> int:
 
 def assemble(grid: VoxelGrid, flow_dir=0, *, check_connectivity: bool = True,
              require_walls: bool = True, device: int | None = None,
-             slabs: int = 1) -> StaggeredSystem:
+             slabs: int = 1, rank: int | None = None, nranks: int = 1) -> StaggeredSystem:
     """Build the staggered operators for a voxel grid on the GPU.
 
     Same signature and errors as operators.py:209-230 plus the backend
     selectors ``device`` (default $VOXSCHUR_DEVICE, else $LOCAL_RANK, else 0)
     and ``slabs``: decompose into that many x-slabs (ranks) with ghost-plane
     exchange inside the fused solver; on one device the
-    ranks run as groups of one cooperative grid.
+    ranks run as groups of one cooperative grid.  With ``rank``/``nranks``
+    (one process per GPU) this process holds only slab ``rank``; call
+    ``connect_ranks`` on every rank before solving.
     """
     if not isinstance(grid, VoxelGrid):
         grid = VoxelGrid(np.asarray(grid))
@@ -195,7 +197,31 @@ def assemble(grid: VoxelGrid, flow_dir=0, *, check_connectivity: bool = True,
     h = grid.physical_length / grid.n
     ctx = C.c_void_p()
     fl = np.ascontiguousarray(grid.fluid, dtype=np.uint8).ravel()
-    _lib.check(_lib.lib.vs_ctx_create2(fl, grid.dim, grid.n, flow_dir, int(check_connectivity),
-                                       int(require_walls), dev, 1.0 / h, 1.0 / h**2, int(slabs),
-                                       C.byref(ctx)))
-    return StaggeredSystem(grid, flow_dir, ctx, dev)
+    if rank is not None and nranks > 1:
+        _lib.check(_lib.lib.vs_ctx_create_rank(fl, grid.dim, grid.n, flow_dir, int(check_connectivity),
+                                               int(require_walls), dev, 1.0 / h, 1.0 / h**2, int(rank),
+                                               int(nranks), C.byref(ctx)))
+    else:
+        _lib.check(_lib.lib.vs_ctx_create2(fl, grid.dim, grid.n, flow_dir, int(check_connectivity),
+                                           int(require_walls), dev, 1.0 / h, 1.0 / h**2, int(slabs),
+                                           C.byref(ctx)))
+    sys_ = StaggeredSystem(grid, flow_dir, ctx, dev)
+    sys_.rank, sys_.nranks = (int(rank), int(nranks)) if rank is not None else (0, 1)
+    return sys_
+
+
+def connect_ranks(sys_: StaggeredSystem, group=None) -> None:
+    """Map every rank's slab into this process (CUDA IPC over NVLink).
+
+    Collective over the ``torch.distributed`` group: each rank contributes
+    its 64-byte arena handle; afterwards the fused solver exchanges ghost
+    planes and reduction partials through peer memory.
+    """
+    import torch.distributed as dist
+
+    h = (C.c_char * 64)()
+    _lib.check(_lib.lib.vs_ipc_handle(sys_._ctx, h))
+    handles = [None] * sys_.nranks
+    dist.all_gather_object(handles, bytes(h), group=group)
+    blob = b"".join(handles)
+    _lib.check(_lib.lib.vs_ipc_attach(sys_._ctx, blob))
