@@ -463,6 +463,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.bar = c->bar;
     P.bar_base = c->bar_base;
     P.npart = c->npart;
+    P.part_self = c->mp() ? c->rank : 0;
     for (int r = 0; r < c->npart; ++r) P.part_peer[r] = c->part_peer[r];
     P.phase_ns = c->phase_ns;
     P.out = c->cglog + li;
@@ -717,6 +718,17 @@ void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
     }
     C->npart = 1;
     C->part_peer[0] = C->part;
+    // VOXSCHUR_EMULATE_RANKS=1: slabs of one process use the multi-process
+    // data flow (a partial buffer per slab arena, every block broadcasting
+    // its sums to all of them), so one GPU exercises that protocol
+    const char *em = getenv("VOXSCHUR_EMULATE_RANKS");
+    if (em && atoi(em) && nranks == 1 && R > 1) {
+        for (int s = 0; s < R; ++s) {
+            const ArenaLayout L = arena_layout(C->slabs[s], C->tb_max, R);
+            C->part_peer[s] = (double *)((char *)C->slabs[s].u[0] - L.u[0] + L.part);
+        }
+        C->npart = R;
+    }
     C->scal_peer[C->rank] = C->scal;
     C->d_groups = C->alloc<CgGroup>(nloc * GROUP_RING);
     CK(cudaMallocHost(&C->h_groups, nloc * GROUP_RING * sizeof(CgGroup)));
@@ -1077,7 +1089,7 @@ static int apply_common(vs_ctx *c, int which, const double *in, double *out) {
     return guarded(c, [&] {
         const bool in_u = (which == 0 || which == 1 || which == 3);
         const bool out_u = (which == 0 || which == 2);
-        c->upload(in_u ? 0 : 1, in_u ? U_IN : P_IN, in);  // owned + ghost planes from the host vector
+        c->upload(in_u ? 0 : 1, in_u ? (int)U_IN : (int)P_IN, in);  // owned + ghost planes from the host vector
         for (int s = c->s0; s < c->s1; ++s) {
             Slab &S = c->slabs[s];
             const double *din = in_u ? S.u[U_IN] : S.p[P_IN];
@@ -1091,7 +1103,7 @@ static int apply_common(vs_ctx *c, int which, const double *in, double *out) {
             }
         }
         CK(cudaGetLastError());
-        c->download(out_u ? 0 : 1, out_u ? U_TMP : P_TMP, out);
+        c->download(out_u ? 0 : 1, out_u ? (int)U_TMP : (int)P_TMP, out);
         c->sync();
     });
 }

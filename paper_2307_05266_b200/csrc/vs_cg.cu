@@ -231,7 +231,10 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
         }
     }
     grid_barrier(P.bar, target, TB);  // starts with __syncthreads (s_warp reuse is safe)
-    const double *part = P.part + (size_t)set * 8 * TB;
+    // own buffer: one per rank (per group when ranks are emulated as groups)
+    const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +
+                         (size_t)set * 8 * TB;
+    __builtin_assume(__isGlobal(part));
     double t[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) t[k] = 0.0;
