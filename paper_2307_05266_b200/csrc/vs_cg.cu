@@ -160,11 +160,12 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
 // all ranks run the same barrier sequence) and each barrier adds the number
 // of participating blocks of all ranks.  One red.release per block, then
 // thread 0 polls.
-// (Measured on B200: ~1.2-1.4 us per barrier for 148-296 blocks, the same
-// as cooperative_groups grid.sync; tools/gridsync_micro.cu.)
 // Polling uses relaxed loads: an acquire load per poll makes ptxas emit an
-// L1 invalidation (CCTL.IVALL) per poll, which wipes the L1 of the other
-// block still computing on the same SM.  One acquire fence after the poll.
+// L1 invalidation (CCTL.IVALL) per poll.  Once the target is seen, one
+// acquire re-read of the counter synchronises with every block's release
+// (the reds form one release sequence); it is 0.13 us cheaper than a
+// fence.acq_rel (B200, 148 x 1024 threads: 1.17 vs 1.30 us per barrier;
+// the unfenced floor is 0.84 us -- tools/gridsync_variants.cu).
 __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, unsigned total_blocks) {
     __syncthreads();
     target += total_blocks;
@@ -172,7 +173,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, un
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
         while ((int)(ld_relaxed(bar) - target) < 0) {
         }
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.gpu.global.u32 t, [%0];\n\t}" ::"l"(bar) : "memory");
     }
     __syncthreads();
 }
@@ -210,8 +211,8 @@ __device__ __forceinline__ void warp_tree(double (&t)[K]) {
 // parallel round trip and reduces them in the same fixed tree, so every
 // block of every rank obtains bitwise-identical totals.
 template <int K>
-__device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams &P, unsigned &target,
-                                         double (*s_warp)[5], double *s_tot) {
+__device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgParams &P, unsigned &target,
+                                              double (*s_warp)[5], double *s_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int TB = P.total_blocks;
     warp_tree<K>(v);
@@ -254,6 +255,72 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
 #pragma unroll
             for (int k = 0; k < K; ++k) s_tot[k] = t[k];
         }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = s_tot[k];
+}
+
+// The per-iteration form (K <= 4).  Block stage through shared memory:
+// every thread stores its K values, then warp k alone reduces component k
+// -- lane i sums threads i, i+32, ..., i+992 in a fixed pairwise tree, one
+// xor butterfly combines the lanes.  The shuffle tree over all 32 warps
+// cost 32 x K x 10 SHFL per block and was SHFL-throughput bound (B200,
+// tools/gridsum_variants.cu: K=4 3.93 -> 2.77 us, K=2 2.95 -> 2.52 us per
+// grid sum).  After the barrier warp k again reduces component k over the
+// blocks (lane i: blocks i, i+32, ... in order; loads issued 8 at a time).
+template <int K>
+__device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams &P, unsigned &target,
+                                         double (*s_val)[CG_THREADS], double *s_tot) {
+    static_assert(K >= 1 && K <= 4, "grid_sum stages at most 4 components");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int TB = P.total_blocks;
+#pragma unroll
+    for (int k = 0; k < K; ++k) s_val[k][threadIdx.x] = v[k];
+    __syncthreads();
+    if (warp < K) {
+        // four chunks of 8 (pairwise within a chunk), then the chunk sums pairwise
+        double c[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            double x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = s_val[warp][lane + 32 * (8 * q + j)];
+#pragma unroll
+            for (int w = 1; w < 8; w *= 2) {
+#pragma unroll
+                for (int j = 0; j < 8; j += 2 * w) x[j] = __dadd_rn(x[j], x[j + w]);
+            }
+            c[q] = x[0];
+        }
+        double t[1] = {__dadd_rn(__dadd_rn(c[0], c[1]), __dadd_rn(c[2], c[3]))};
+        warp_tree<1>(t);
+        if (lane < P.npart) {  // lane p stores to rank p's buffer
+            double *dst =
+                P.part_peer[lane] + (size_t)set * 8 * TB + (size_t)(P.block_base + blockIdx.x) * 8 + warp;
+            __builtin_assume(__isGlobal(dst));
+            *dst = t[0];
+        }
+    }
+    grid_barrier(P.bar, target, TB);  // starts with __syncthreads (s_val reuse is safe)
+    if (warp < K) {
+        // own buffer: one per rank (per group when ranks are emulated as groups)
+        const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +
+                             (size_t)set * 8 * TB + warp;
+        __builtin_assume(__isGlobal(part));
+        double t[1] = {0.0};
+        for (int b0 = 0; b0 < TB; b0 += 32 * 8) {
+            double w[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int b = b0 + lane + 32 * j;
+                w[j] = b < TB ? __ldcg(part + (size_t)b * 8) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) t[0] = __dadd_rn(t[0], w[j]);
+        }
+        warp_tree<1>(t);
+        if (lane == 0) s_tot[warp] = t[0];
     }
     __syncthreads();
 #pragma unroll
@@ -311,6 +378,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
     __shared__ double s_tab[40];
     __shared__ double s_warp[CG_THREADS / 32][5];
     __shared__ double s_tot[5];
+    __shared__ __align__(16) double s_val[4][CG_THREADS];  // grid_sum staging (32 KB)
     __shared__ CgGroup G;  // this block's slab (group)
     const int grp = P.group_base + blockIdx.x / P.bpg;
     if (threadIdx.x == 0) G = P.groups[grp];
@@ -344,7 +412,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
     if (PROJ) {
         double v[1] = {0.0};
         for (uint32_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], G.rhs[i]);
-        grid_sum<1>(v, 0, P, gen, s_warp, s_tot);
+        grid_sum<1>(v, 0, P, gen, s_val, s_tot);
         mu_rhs = v[0] / P.m_global;
     }
     {
@@ -380,7 +448,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
             v[3] = __dadd_rn(v[3], zi);
             v[4] = __dadd_rn(v[4], ri);
         }
-        grid_sum<5>(v, 1, P, gen, s_warp, s_tot);
+        grid_sum_shfl<5>(v, 1, P, gen, s_warp, s_tot);
         if (PROJ) {
             mu = v[3] / P.m_global;
             v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
@@ -448,7 +516,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                 dnew[i] = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dold[i]));
             }
             const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            grid_sum<1>(v1, 2, P, gen, s_warp, s_tot);
+            grid_sum<1>(v1, 2, P, gen, s_val, s_tot);
             const uint64_t t2 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             const double dq = v1[0];
             if (dq <= 0.0) { status = 2; sval = dq; sat = it; break; }
@@ -496,7 +564,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                 }
             }
             const uint64_t t3 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            grid_sum<KL>(v, 3, P, gen, s_warp, s_tot);
+            grid_sum<KL>(v, 3, P, gen, s_val, s_tot);
             if (P.phase_ns && threadIdx.x == 0) {
                 const uint64_t t4 = gtimer();
                 ph[0] += t1 - t0;
@@ -560,10 +628,12 @@ CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     const int ns = 2 * dim;
-    size_t budget = std::min<size_t>(CG_SMEM_BUDGET, (size_t)maxopt);
-    if (const char *e = getenv("VOXSCHUR_SMEM_KB")) budget = std::min<size_t>(budget, (size_t)atoi(e) * 1024);
     for (int tier = 2; tier >= 1; --tier) {
         const void *fn = pcg_fn(dim, op, tier);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, fn);  // static smem (grid_sum staging, tables)
+        size_t budget = std::min<size_t>(CG_SMEM_BUDGET, (size_t)maxopt - fa.sharedSizeBytes);
+        if (const char *e = getenv("VOXSCHUR_SMEM_KB")) budget = std::min<size_t>(budget, (size_t)atoi(e) * 1024);
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CG_THREADS, budget);
