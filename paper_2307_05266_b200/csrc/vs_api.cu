@@ -60,8 +60,8 @@ namespace {
 // ----------------------------------------------------------------- slabs
 // Vector slots of a slab.  Velocity slots have m_all[0] entries, pressure
 // slots m_all[1]; owned DOFs first, ghost-plane DOFs after.
-enum USlot { U_RHS, U_W, U_ITER, U_F, U_R, U_Z, U_D0, U_D1, U_TMP, U_IN, NU };
-enum PSlot { P_X, P_R, P_D, P_Z, P_Q, P_B, P_SR, P_SZ, P_SD0, P_SD1, P_TMP, P_IN, NP };
+enum USlot { U_RHS, U_W, U_ITER, U_F, U_R, U_Z, U_D0, U_D1, U_CQ, U_TMP, U_IN, NU };
+enum PSlot { P_X, P_R, P_D, P_Z, P_Q, P_B, P_SR, P_SZ, P_SD0, P_SD1, P_SQ, P_TMP, P_IN, NP };
 constexpr int FP = 3;  // family index of the pressure (velocity components are 0..dim-1)
 
 // One group of the decomposition: a slab of x-planes [x_lo, x_hi) with one
@@ -434,6 +434,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         G.z = op == 0 ? S.u[U_Z] : S.p[P_SZ];
         G.d0 = op == 0 ? S.u[U_D0] : S.p[P_SD0];
         G.d1 = op == 0 ? S.u[U_D1] : S.p[P_SD1];
+        G.q = op == 0 ? S.u[U_CQ] : S.p[P_SQ];
         if (R > 1) {
             Slab &lo = c->slabs[(s - 1 + R) % R], &hi = c->slabs[(s + 1) % R];
             G.zpeer[0] = op == 0 ? lo.u[U_Z] : lo.p[P_SZ];

@@ -4,8 +4,9 @@
 //   P1  d = (z - mu) + beta d_old        (z stored by P2, mean-projected for S_hat)
 //       q = op(d), neighbour d recomputed from z/d_old -> no extra pass
 //       partial d.q                                              -> barrier 1
-//   P2  q = op(d) from the stored d; x -= alpha d; r -= alpha q;
-//       z = M^-1 r (stored); partials r.z, z.z, r.r, sum z, sum r -> barrier 2
+//   P2  x -= alpha d; r -= alpha q (q stored by P1: P2 is a pure stream, no
+//       gathers or rank lookups); z = M^-1 r (stored);
+//       partials r.z, z.z (+ sum z, sum r when projected)       -> barrier 2
 // Scalars live in registers of every block: each block reduces the same
 // per-block partials in the same fixed order, so alpha/beta/mu and the
 // convergence decision are bitwise identical everywhere (deterministic for
@@ -16,9 +17,14 @@
 // dadd(z, dmul(beta, d))) with explicit round-to-nearest intrinsics.
 //
 // DRAM bytes per DOF per iteration (8 B each): P1 reads z, d_old, record and
-// writes d; P2 reads d, x, r, record and writes x, r, z  -> 88 B (plus
-// L2-resident bitmask words for the neighbour ranks).
+// writes d, q; P2 reads d, q, x, r, record and writes x, r, z  -> 104 B (less
+// whatever stays in L2 and the smem DOF cache), plus the L2-resident bitmask
+// words for the neighbour ranks.  Storing q costs 16 B/DOF but halves the
+// rank lookups and stencil work, which bound the passes (issue-bound at
+// ~280 SASS instructions per DOF per pass before; 36 % of them rank lookups,
+// ncu source counters, profiles/).
 #include <cstdlib>
+#include <type_traits>
 
 #include "vs_device.cuh"
 #include "vs_internal.h"
@@ -30,36 +36,39 @@ namespace vs {
 // (x+, x-, [y+, y-,] z+, z-)   (operators.py:269-271: d = 0..dim-1, s = +1, -1)
 // (nx = extent of the local x axis: n for a whole-domain group, slab planes
 // + 2 ghost planes otherwise -- owned DOFs of a slab never wrap in x).
-// The tangential neighbours share the DOF's bit position, so their ranks are
-// word + popc(mask & below(b)) at a word offset from the DOF's own word.
-template <int DIM>
+// Presence comes from the record.  The z neighbours lie on the DOF's own
+// line, so they are ranks i +- 1 except across the periodic wrap (one meta
+// load).  The tangential neighbours share the DOF's bit position, so their
+// ranks are base + popc(mask & below(b)) of the word at a fixed offset.
+template <int DIM, int OP>
 __device__ __forceinline__ void neighbour_ranks(const uint2 *__restrict__ meta, int nw, int n, int nx,
-                                                uint64_t rc, uint32_t (&nr)[2 * DIM]) {
+                                                uint64_t rc, uint32_t i, uint32_t (&nr)[2 * DIM]) {
     const int z = rec_z(rc), y = rec_y(rc), x = rec_x(rc);
     const uint32_t b = (uint32_t)z & 31u, below = (1u << b) - 1u;
     const int lineW = (DIM == 3 ? x * n + y : x) * nw;  // word 0 of the DOF's line
     const int w0 = lineW + (z >> 5);
     const int planeW = (DIM == 3 ? n : 1) * nw;           // words per x-plane
-    auto tang = [&](int idx) -> uint32_t {
+    auto tang = [&](int s, int idx) -> uint32_t {
+        if (!rec_has_nb<OP>(rc, s)) return ABSENT;
         const uint2 m = __ldg(meta + idx);
-        const uint32_t rk = m.y + (uint32_t)__popc(m.x & below);
-        return ((m.x >> b) & 1u) ? rk : ABSENT;
+        return m.y + (uint32_t)__popc(m.x & below);
     };
-    nr[0] = tang(w0 + ((x == nx - 1) ? -(nx - 1) * planeW : planeW));
-    nr[1] = tang(w0 + ((x == 0) ? (nx - 1) * planeW : -planeW));
+    nr[0] = tang(0, w0 + ((x == nx - 1) ? -(nx - 1) * planeW : planeW));
+    nr[1] = tang(1, w0 + ((x == 0) ? (nx - 1) * planeW : -planeW));
     if (DIM == 3) {
-        nr[2] = tang(w0 + ((y == n - 1) ? -(n - 1) * nw : nw));
-        nr[3] = tang(w0 + ((y == 0) ? (n - 1) * nw : -nw));
+        nr[2] = tang(2, w0 + ((y == n - 1) ? -(n - 1) * nw : nw));
+        nr[3] = tang(3, w0 + ((y == 0) ? (n - 1) * nw : -nw));
     }
-    const int zp = (z == n - 1) ? 0 : z + 1, zm = (z == 0) ? n - 1 : z - 1;
-    auto along = [&](int zz) -> uint32_t {
+    const bool hp = rec_has_nb<OP>(rc, 2 * DIM - 2), hm = rec_has_nb<OP>(rc, 2 * DIM - 1);
+    const bool top = (z == n - 1), bot = (z == 0);
+    uint32_t rw = 0;
+    if ((top && hp) || (bot && hm)) {  // periodic wrap: cell 0 (from the top) or n-1 (from the bottom)
+        const int zz = top ? 0 : n - 1;
         const uint2 m = __ldg(meta + lineW + (zz >> 5));
-        const uint32_t bb = (uint32_t)zz & 31u;
-        const uint32_t rk = m.y + (uint32_t)__popc(m.x & ((1u << bb) - 1u));
-        return ((m.x >> bb) & 1u) ? rk : ABSENT;
-    };
-    nr[2 * DIM - 2] = along(zp);
-    nr[2 * DIM - 1] = along(zm);
+        rw = m.y + (uint32_t)__popc(m.x & ((1u << (zz & 31)) - 1u));
+    }
+    nr[2 * DIM - 2] = hp ? (top ? rw : i + 1) : ABSENT;
+    nr[2 * DIM - 1] = hm ? (bot ? rw : i - 1) : ABSENT;
 }
 
 struct Tabs {
@@ -279,10 +288,12 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
     for (int k = 0; k < K; ++k) s_val[k][threadIdx.x] = v[k];
     __syncthreads();
     if (warp < K) {
-        // four chunks of 8 (pairwise within a chunk), then the chunk sums pairwise
-        double c[4];
+        // chunks of 8 (pairwise within a chunk), then the chunk sums pairwise
+        constexpr int NC = CG_THREADS / 256;
+        static_assert(NC == 2 || NC == 4, "grid_sum block stage: 512 or 1024 threads");
+        double c[NC];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < NC; ++q) {
             double x[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) x[j] = s_val[warp][lane + 32 * (8 * q + j)];
@@ -293,7 +304,11 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
             }
             c[q] = x[0];
         }
-        double t[1] = {__dadd_rn(__dadd_rn(c[0], c[1]), __dadd_rn(c[2], c[3]))};
+        double t[1];
+        if constexpr (NC == 4)
+            t[0] = __dadd_rn(__dadd_rn(c[0], c[1]), __dadd_rn(c[2], c[3]));
+        else
+            t[0] = __dadd_rn(c[0], c[1]);
         warp_tree<1>(t);
         if (lane < P.npart) {  // lane p stores to rank p's buffer
             double *dst =
@@ -367,7 +382,7 @@ __device__ __forceinline__ void fetch_dof(const CgParams &P, const CgGroup &G, c
         __builtin_assume(__isGlobal(rec));
         rc = rec[i];
     }
-    neighbour_ranks<DIM>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, nr);
+    neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, i, nr);
 }
 
 template <int DIM, int OP, int TIER>
@@ -397,13 +412,14 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
     const int fam_p = 0;
     const uint32_t tid = (blockIdx.x % P.bpg) * CG_THREADS + threadIdx.x;
     const uint32_t stride = P.bpg * CG_THREADS;
-    double *x = G.x, *r = G.r, *z = G.z;
+    double *x = G.x, *r = G.r, *z = G.z, *q = G.q;
     const bool halo = G.zpeer[0] != nullptr;  // multi-slab run: ghost-plane exchange
     // pointers come from shared memory: tell the compiler they are global
     // (LDG/STG instead of generic LD/ST)
     __builtin_assume(__isGlobal(x));
     __builtin_assume(__isGlobal(r));
     __builtin_assume(__isGlobal(z));
+    __builtin_assume(__isGlobal(q));
     const double inv_h = P.inv_h, inv_h2 = P.inv_h2;
 
     // ---- setup (krylov.py:102-119): project rhs; r = op(x0) - rhs; z = M^-1 r;
@@ -423,7 +439,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
             const uint64_t rc = G.rec[i];
             uint32_t nr[NS];
             if (x0 || (TIER == 2 && k < kc))
-                neighbour_ranks<DIM>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, nr);
+                neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, i, nr);
             if (k < kc) cache.put(k, rc, nr);
             double ax = 0.0, xi = 0.0;
             if (x0) {
@@ -471,57 +487,71 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
         for (int64_t it = 0; it < P.max_iter; ++it) {
             if (rz < 0.0) { status = 1; sval = rz; sat = it; break; }
             if (rz == 0.0) { conv = true; break; }
-            const bool first = (it == 0);
             const uint64_t t0 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            // ---- P1: d = z - mu + beta d_old, q = op(d), d.q
+            // ---- P1: d = z - mu + beta d_old, q = op(d), d.q  (instantiated
+            // separately for the first iteration, where d = z - mu)
             double v1[1] = {0.0};
-            uint32_t k = 0;
-            for (uint32_t i = tid; i < m; i += stride, ++k) {
-                const uint32_t ip = i + P.pf_dist * stride;
-                if (P.pf_dist && ip < m) {  // stream the centre vectors pf_dist strides ahead
-                    if (k + 2 >= kc) prefetch_l2(G.rec + ip);
-                    prefetch_l2(z + ip);
-                    if (!first) prefetch_l2(dold + ip);
-                }
-                double zc = z[i];
-                const double dc = first ? 0.0 : dold[i];
-                uint64_t rc;
-                uint32_t nr[NS];
-                fetch_dof<DIM, OP, TIER>(P, G, cache, k, kc, i, rc, nr);
-                double zn[NS], dn[NS];
+            auto pass1 = [&](auto first_c) {
+                const bool first = first_c;  // constant-folded for std::bool_constant
+                uint32_t k = 0;
+                for (uint32_t i = tid; i < m; i += stride, ++k) {
+                    const uint32_t ip = i + P.pf_dist * stride;
+                    if (P.pf_dist && ip < m) {  // stream the centre vectors pf_dist strides ahead
+                        if (k + 2 >= kc) prefetch_l2(G.rec + ip);
+                        prefetch_l2(z + ip);
+                        if (!first) prefetch_l2(dold + ip);
+                    }
+                    double zc = z[i];
+                    const double dc = first ? 0.0 : dold[i];
+                    uint64_t rc;
+                    uint32_t nr[NS];
+                    fetch_dof<DIM, OP, TIER>(P, G, cache, k, kc, i, rc, nr);
+                    double zn[NS], dn[NS];
 #pragma unroll
-                for (int s = 0; s < NS; ++s) {  // unconditional loads (absent -> own index)
-                    const uint32_t j = nr[s] != ABSENT ? nr[s] : i;
-                    zn[s] = z[j];
-                    dn[s] = first ? 0.0 : dold[j];
-                }
-                if (PROJ) zc = __dsub_rn(zc, mu);
-                const double di = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dc));
-                double vn[NS];
+                    for (int s = 0; s < NS; ++s) {  // unconditional loads (absent -> own index)
+                        const uint32_t j = nr[s] != ABSENT ? nr[s] : i;
+                        zn[s] = z[j];
+                        dn[s] = first ? 0.0 : dold[j];
+                    }
+                    if (PROJ) zc = __dsub_rn(zc, mu);
+                    const double di = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dc));
+                    double vn[NS];
 #pragma unroll
-                for (int s = 0; s < NS; ++s) {
-                    double zj = zn[s];
-                    if (PROJ) zj = __dsub_rn(zj, mu);
-                    const double dj = first ? zj : __dadd_rn(zj, __dmul_rn(beta, dn[s]));
-                    vn[s] = nr[s] == ABSENT ? 0.0 : dj;
+                    for (int s = 0; s < NS; ++s) {
+                        double zj = zn[s];
+                        if (PROJ) zj = __dsub_rn(zj, mu);
+                        const double dj = first ? zj : __dadd_rn(zj, __dmul_rn(beta, dn[s]));
+                        // A needs 0.0 at absent slots (left fold); S_hat's absent faces
+                        // carry weight 0.0 (op_value), so the clamped value is harmless
+                        vn[s] = (OP == 0 && nr[s] == ABSENT) ? 0.0 : dj;
+                    }
+                    const double qi = op_value<DIM, OP>(rc, di, vn, T, inv_h, inv_h2);
+                    dnew[i] = di;
+                    q[i] = qi;
+                    v1[0] = __dadd_rn(v1[0], __dmul_rn(di, qi));
                 }
-                const double qi = op_value<DIM, OP>(rc, di, vn, T, inv_h, inv_h2);
-                dnew[i] = di;
-                v1[0] = __dadd_rn(v1[0], __dmul_rn(di, qi));
-            }
-            // ghost-plane d, recomputed exactly as the owning slab computes it
-            for (uint32_t i = m + tid; i < m_all; i += stride) {
-                double zc = z[i];
-                if (PROJ) zc = __dsub_rn(zc, mu);
-                dnew[i] = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dold[i]));
-            }
+                // ghost-plane d, recomputed exactly as the owning slab computes it
+                for (uint32_t i = m + tid; i < m_all; i += stride) {
+                    double zc = z[i];
+                    if (PROJ) zc = __dsub_rn(zc, mu);
+                    dnew[i] = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dold[i]));
+                }
+            };
+            // peeling the first iteration pays for S_hat (B200, C2: 63.8 -> 57.3
+            // us/it) but not for A (131.5 -> 137 us/it: register allocation)
+            if (OP == 1 && it == 0)
+                pass1(std::true_type{});
+            else if (OP == 1)
+                pass1(std::false_type{});
+            else
+                pass1(it == 0);
             const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             grid_sum<1>(v1, 2, P, gen, s_val, s_tot);
             const uint64_t t2 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             const double dq = v1[0];
             if (dq <= 0.0) { status = 2; sval = dq; sat = it; break; }
             const double alpha = rz / dq;
-            // ---- P2: q = op(d); x -= alpha d; r -= alpha q; z = M^-1 r; sums
+            // ---- P2: x -= alpha d; r -= alpha q; z = M^-1 r; sums
             // per-iteration sums: r.z, z.z (+ sum z, sum r when projected).
             // Inner solves stop on the preconditioned norm (schur.py:207-210),
             // so |r| is not needed: z = r * (positive finite inverse diagonal)
@@ -529,26 +559,26 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
             constexpr int KL = PROJ ? 4 : 2;
             double v[KL];
 #pragma unroll
-            for (int q = 0; q < KL; ++q) v[q] = 0.0;
-            k = 0;
+            for (int s = 0; s < KL; ++s) v[s] = 0.0;
+            uint32_t k = 0;
             for (uint32_t i = tid; i < m; i += stride, ++k) {
                 const uint32_t ip = i + P.pf_dist * stride;
                 if (P.pf_dist && ip < m) {
                     if (k + 2 >= kc) prefetch_l2(G.rec + ip);
                     prefetch_l2(dnew + ip);
+                    prefetch_l2(q + ip);
                     prefetch_l2(x + ip);
                     prefetch_l2(r + ip);
                 }
-                const double di = dnew[i], xo = x[i], ro = r[i];
+                const double di = dnew[i], qi = q[i], xo = x[i], ro = r[i];
                 uint64_t rc;
-                uint32_t nr[NS];
-                fetch_dof<DIM, OP, TIER>(P, G, cache, k, kc, i, rc, nr);
-                double vn[NS];
-#pragma unroll
-                for (int s = 0; s < NS; ++s) vn[s] = dnew[nr[s] != ABSENT ? nr[s] : i];
-#pragma unroll
-                for (int s = 0; s < NS; ++s) vn[s] = nr[s] == ABSENT ? 0.0 : vn[s];
-                const double qi = op_value<DIM, OP>(rc, di, vn, T, inv_h, inv_h2);
+                if (k < kc) {
+                    rc = cache.rec[k * CG_THREADS + threadIdx.x];
+                } else {
+                    const uint64_t *rec = G.rec;
+                    __builtin_assume(__isGlobal(rec));
+                    rc = rec[i];
+                }
                 const double xi = __dsub_rn(xo, __dmul_rn(alpha, di));
                 const double ri = __dsub_rn(ro, __dmul_rn(alpha, qi));
                 const double zi = __dmul_rn(ri, jacobi_inv<OP>(rc, T));

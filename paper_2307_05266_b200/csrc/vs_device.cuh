@@ -26,7 +26,9 @@ namespace vs {
 constexpr uint32_t ABSENT = 0xFFFFFFFFu;
 
 // ---- record bit layout ------------------------------------------------
-// z:0..10  y:11..21  x:22..32  comp:33..34  vcode:36..39  pcodes:40..57
+// z:0..10  y:11..21  x:22..32  comp:33..34  vcode:36..39
+// velocity: neighbour presence 40..45 (slot order x+, x-, [y+, y-,] z+, z-)
+// pressure: face codes 40..57 (nonzero <=> the neighbour cell is fluid)
 __host__ __device__ __forceinline__ uint64_t make_rec(int x, int y, int z, int comp) {
     return (uint64_t)z | ((uint64_t)y << 11) | ((uint64_t)x << 22) | ((uint64_t)comp << 33);
 }
@@ -40,6 +42,12 @@ __device__ __forceinline__ int rec_vcode(uint64_t r) { return (int)((r >> 36) & 
 __device__ __forceinline__ int rec_pin(uint64_t r, int a) { return (int)((r >> (40 + 3 * a)) & 7); }
 __device__ __forceinline__ int rec_pout(uint64_t r, int a) { return (int)((r >> (49 + 3 * a)) & 7); }
 __device__ __forceinline__ uint32_t rec_pkey(uint64_t r) { return (uint32_t)((r >> 40) & 0x3FFFF); }
+// neighbour in slot s = 2a + (minus) present? (OP 0 velocity, OP 1 pressure)
+template <int OP>
+__device__ __forceinline__ bool rec_has_nb(uint64_t r, int s) {
+    if (OP == 0) return (r >> (40 + s)) & 1u;
+    return (s & 1) ? rec_pin(r, s >> 1) != 0 : rec_pout(r, s >> 1) != 0;
+}
 
 struct Geo {
     int dim, n, nw, nlines;

@@ -8,7 +8,10 @@
 
 namespace vs {
 
-constexpr int CG_THREADS = 1024;
+#ifndef VS_CG_THREADS
+#define VS_CG_THREADS 1024
+#endif
+constexpr int CG_THREADS = VS_CG_THREADS;
 constexpr int RED_THREADS = 256;
 constexpr int RED_MAX_BLOCKS = 592;
 constexpr int VS_MAX_SLABS = 16;
@@ -30,7 +33,7 @@ struct CgGroup {
     int nx;                 // local x extent (n when the group is the whole domain)
     uint32_t m_own, m_all;  // owned DOFs, owned + ghost
     const double *rhs, *x0;
-    double *x, *r, *z, *d0, *d1;
+    double *x, *r, *z, *d0, *d1, *q;
     // halo: side s = 0 sends the first owned plane to the lower neighbour's
     // ghost_hi, s = 1 the last owned plane to the upper neighbour's ghost_lo;
     // per family f, local range [sbeg, send) -> zpeer[s][sdst + (i - sbeg)]

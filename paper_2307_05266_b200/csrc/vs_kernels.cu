@@ -89,7 +89,14 @@ __global__ void k_vel_records(Geo g, int a, int64_t nwords, uint64_t *rec) {
         bits &= bits - 1;
         const Cell c = word_cell(g, word, b);
         const int code = face_code(g, a, c);
-        rec[m.y + k] = make_rec(c.x, c.y, c.z, a) | ((uint64_t)code << 36);
+        // presence of the 2*dim same-component neighbour faces, slot order
+        // (d, s = +1, -1) -> bits 40 + 2d + (s < 0) (the fused CG's rank lookups)
+        uint64_t pres = 0;
+        for (int dd = 0; dd < g.dim; ++dd)
+            for (int si = 0; si < 2; ++si)
+                if (rank_at(g.vmeta[a], g, shifted(c, iaxis(g.dim, dd), si == 0 ? 1 : -1, g)) != ABSENT)
+                    pres |= 1ull << (40 + 2 * dd + si);
+        rec[m.y + k] = make_rec(c.x, c.y, c.z, a) | ((uint64_t)code << 36) | pres;
         ++k;
     }
 }
