@@ -1,7 +1,16 @@
 import os
 import sys
 
-import numpy as np
+# The golden fixtures were produced with a single-threaded OpenBLAS
+# (tests/golden/make_golden.py); a threaded ddot splits the sum differently,
+# so the oracle's bitwise pins only hold with one BLAS thread.
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ[_v] = "1"
+
+import numpy as np  # noqa: E402
+from threadpoolctl import threadpool_limits  # noqa: E402
+
+threadpool_limits(1)
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
