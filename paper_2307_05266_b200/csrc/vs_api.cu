@@ -463,6 +463,8 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.part = c->part;
     P.bar = c->bar;
     P.bar_base = c->bar_base;
+    P.ll_epoch = c->bar_base + 1;
+    P.fence_sys = c->mp() ? 1 : 0;
     P.npart = c->npart;
     P.part_self = c->mp() ? c->rank : 0;
     for (int r = 0; r < c->npart; ++r) P.part_peer[r] = c->part_peer[r];
@@ -626,7 +628,7 @@ ArenaLayout arena_layout(const Slab &S, int64_t tb_max, int R) {
     };
     for (int k = 0; k < NU; ++k) L.u[k] = take(std::max<int64_t>(1, S.m_all[0]) * sizeof(double));
     for (int k = 0; k < NP; ++k) L.p[k] = take(std::max<int64_t>(1, S.m_all[1]) * sizeof(double));
-    L.part = take((size_t)4 * 8 * tb_max * sizeof(double));
+    L.part = take((size_t)4 * 8 * tb_max * 2 * sizeof(uint64_t));  // flag-word slots (vs_cg.cu)
     L.scal = take((size_t)Q_COUNT * R * sizeof(double));
     L.bar = take(4 * sizeof(unsigned));
     L.bytes = off;
@@ -716,6 +718,8 @@ void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
             C->bar_base = C->bar + 1;
             CK(cudaMemsetAsync(C->bar, 0, 4 * sizeof(unsigned), C->stream));
         }
+        // grid-sum slots start at epoch 0; the first sum uses epoch 1
+        CK(cudaMemsetAsync(base + L.part, 0, L.scal - L.part, C->stream));
     }
     C->npart = 1;
     C->part_peer[0] = C->part;

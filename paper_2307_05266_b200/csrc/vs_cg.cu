@@ -148,43 +148,78 @@ __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-// ------------------------------------------------------------- grid barrier
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// ------------------------------------------------------- grid reductions
+// Flag-in-word ("LL") grid sums.  A block's partial is a double split into
+// two 8-byte words {epoch:32 | half:32}; an 8-byte store is single-copy
+// atomic, so a reader that sees the current epoch in both words has the
+// value -- no separate arrival counter, no release/acquire round trip just
+// to publish a scalar.  Readers poll the slots of all blocks directly.
+// Every grid sum of every launch has its own epoch (monotonic, carried
+// across launches in *P.ll_epoch), so stale slots never match.
+//
+// ORDER = the sum also orders this block's earlier global stores (z of P2,
+// the setup pass) before any reader's later loads: writers fence (release)
+// before the flag store, readers fence (acquire, which also invalidates L1)
+// after seeing the flags.  The sum after P1 needs no ordering: P2 reads only
+// d, q of its own DOFs (written by the same thread), and a block posts its
+// partial only after its P1 loads have returned (they feed the partial), so
+// P2's stores cannot race them.
+__device__ __forceinline__ void fence_acq_rel(bool sys) {
+    if (sys)
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
-// bar = monotonic arrival counter shared by every block of every rank; it is
-// never reset.  Each launch starts from *P.bar_base (the previous launch's
-// final target, written back by its block 0 -- identical on every rank, since
-// all ranks run the same barrier sequence) and each barrier adds the number
-// of participating blocks of all ranks.  One red.release per block, then
-// thread 0 polls.
-// Polling uses relaxed loads: an acquire load per poll makes ptxas emit an
-// L1 invalidation (CCTL.IVALL) per poll.  Once the target is seen, one
-// acquire re-read of the counter synchronises with every block's release
-// (the reds form one release sequence); it is 0.13 us cheaper than a
-// fence.acq_rel (B200, 148 x 1024 threads: 1.17 vs 1.30 us per barrier;
-// the unfenced floor is 0.84 us -- tools/gridsync_variants.cu).
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, unsigned total_blocks) {
-    __syncthreads();
-    target += total_blocks;
-    if (threadIdx.x == 0) {
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-        while ((int)(ld_relaxed(bar) - target) < 0) {
+__device__ __forceinline__ void st_ll(uint64_t *p, double v, unsigned e) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long hi = (unsigned long long)e << 32;
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(hi | (b & 0xffffffffull)),
+                 "l"(hi | (b >> 32))
+                 : "memory");
+}
+
+// slot (set, component k, block b): two words
+__device__ __forceinline__ uint64_t *ll_slot(double *buf, int set, int k, int TB, int b) {
+    return reinterpret_cast<uint64_t *>(buf) + ((size_t)(set * 8 + k) * TB + b) * 2;
+}
+
+// Warp-wide: sum component k over all TB blocks in a fixed order (lane i:
+// blocks i, i+32, ... in chunks of 8, then an xor butterfly).  Polls until
+// every slot carries epoch e.  Result in every lane.
+__device__ __forceinline__ double ll_collect(const uint64_t *row, int TB, unsigned e) {
+    const int lane = threadIdx.x & 31;
+    double t = 0.0;
+    for (int b0 = 0; b0 < TB; b0 += 32 * 8) {
+        double w[8];
+        unsigned pend = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            w[j] = 0.0;
+            if (b0 + lane + 32 * j < TB) pend |= 1u << j;
         }
-        asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.gpu.global.u32 t, [%0];\n\t}" ::"l"(bar) : "memory");
+        while (pend) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (pend & (1u << j)) {
+                    unsigned long long lo, hi;
+                    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                                 : "=l"(lo), "=l"(hi)
+                                 : "l"(row + (size_t)(b0 + lane + 32 * j) * 2)
+                                 : "memory");
+                    if ((unsigned)(lo >> 32) == e && (unsigned)(hi >> 32) == e) {
+                        w[j] = __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+                        pend &= ~(1u << j);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t = __dadd_rn(t, w[j]);
     }
-    __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(~0u, t, o));
+    return t;
 }
 
 // Warp 0 combines the per-warp values s_warp[w][k] (w < CG_THREADS/32) with
@@ -212,18 +247,26 @@ __device__ __forceinline__ void warp_tree(double (&t)[K]) {
     }
 }
 
+// own partial buffer: one per rank (per group when ranks are emulated as groups)
+__device__ __forceinline__ double *ll_own(const CgParams &P) {
+    double *b = P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part;
+    __builtin_assume(__isGlobal(b));
+    return b;
+}
+
 // Deterministic grid-wide sum of K values over every block of every rank.
-// Block g (global index block_base + blockIdx.x) writes its K sums into slot
-// g of partial set `set` of EVERY rank's partial buffer (peer stores on a
-// multi-GPU run; one buffer when the ranks are groups of one launch).  After
-// the barrier each block reads all blocks' sums from its own buffer in one
-// parallel round trip and reduces them in the same fixed tree, so every
-// block of every rank obtains bitwise-identical totals.
-template <int K>
-__device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgParams &P, unsigned &target,
+// Block g (global index block_base + blockIdx.x) publishes its K sums into
+// slot g of partial set `set` of EVERY rank's buffer (peer stores on a
+// multi-GPU run; one buffer when the ranks are groups of one launch); every
+// block then reduces all blocks' slots of its own buffer in the same fixed
+// tree, so every block of every rank obtains bitwise-identical totals.
+// This form (K <= 5, setup only) stages the block through warp shuffles.
+template <int K, bool ORDER>
+__device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgParams &P, unsigned &ep,
                                               double (*s_warp)[5], double *s_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int TB = P.total_blocks;
+    ++ep;
     warp_tree<K>(v);
     if (lane == 0) {
 #pragma unroll
@@ -234,36 +277,15 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
         double t[K];
         warp0_combine<K>(s_warp, t);
         if (lane < P.npart) {  // lane p stores to rank p's buffer
-            double *dst = P.part_peer[lane] + (size_t)set * 8 * TB + (size_t)(P.block_base + blockIdx.x) * 8;
-            __builtin_assume(__isGlobal(dst));
+            if (ORDER) fence_acq_rel(P.fence_sys);
 #pragma unroll
-            for (int k = 0; k < K; ++k) dst[k] = t[k];
+            for (int k = 0; k < K; ++k) st_ll(ll_slot(P.part_peer[lane], set, k, TB, P.block_base + blockIdx.x), t[k], ep);
         }
     }
-    grid_barrier(P.bar, target, TB);  // starts with __syncthreads (s_warp reuse is safe)
-    // own buffer: one per rank (per group when ranks are emulated as groups)
-    const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +
-                         (size_t)set * 8 * TB;
-    __builtin_assume(__isGlobal(part));
-    double t[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) t[k] = 0.0;
-    for (int b = threadIdx.x; b < TB; b += CG_THREADS) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) t[k] = __dadd_rn(t[k], __ldcg(part + b * 8 + k));
-    }
-    warp_tree<K>(t);
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) s_warp[warp][k] = t[k];
-    }
-    __syncthreads();
-    if (warp == 0) {
-        warp0_combine<K>(s_warp, t);
-        if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) s_tot[k] = t[k];
-        }
+    if (warp < K) {
+        const double t = ll_collect(ll_slot(ll_own(P), set, warp, TB, 0), TB, ep);
+        if (ORDER) fence_acq_rel(P.fence_sys);
+        if (lane == 0) s_tot[warp] = t;
     }
     __syncthreads();
 #pragma unroll
@@ -275,15 +297,15 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
 // -- lane i sums threads i, i+32, ..., i+992 in a fixed pairwise tree, one
 // xor butterfly combines the lanes.  The shuffle tree over all 32 warps
 // cost 32 x K x 10 SHFL per block and was SHFL-throughput bound (B200,
-// tools/gridsum_variants.cu: K=4 3.93 -> 2.77 us, K=2 2.95 -> 2.52 us per
-// grid sum).  After the barrier warp k again reduces component k over the
-// blocks (lane i: blocks i, i+32, ... in order; loads issued 8 at a time).
-template <int K>
-__device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams &P, unsigned &target,
+// tools/gridsum_variants.cu).  Warp k then publishes component k and
+// collects it over the blocks.
+template <int K, bool ORDER>
+__device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams &P, unsigned &ep,
                                          double (*s_val)[CG_THREADS], double *s_tot) {
     static_assert(K >= 1 && K <= 4, "grid_sum stages at most 4 components");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int TB = P.total_blocks;
+    ++ep;
 #pragma unroll
     for (int k = 0; k < K; ++k) s_val[k][threadIdx.x] = v[k];
     __syncthreads();
@@ -311,31 +333,12 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
             t[0] = __dadd_rn(c[0], c[1]);
         warp_tree<1>(t);
         if (lane < P.npart) {  // lane p stores to rank p's buffer
-            double *dst =
-                P.part_peer[lane] + (size_t)set * 8 * TB + (size_t)(P.block_base + blockIdx.x) * 8 + warp;
-            __builtin_assume(__isGlobal(dst));
-            *dst = t[0];
+            if (ORDER) fence_acq_rel(P.fence_sys);
+            st_ll(ll_slot(P.part_peer[lane], set, warp, TB, P.block_base + blockIdx.x), t[0], ep);
         }
-    }
-    grid_barrier(P.bar, target, TB);  // starts with __syncthreads (s_val reuse is safe)
-    if (warp < K) {
-        // own buffer: one per rank (per group when ranks are emulated as groups)
-        const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +
-                             (size_t)set * 8 * TB + warp;
-        __builtin_assume(__isGlobal(part));
-        double t[1] = {0.0};
-        for (int b0 = 0; b0 < TB; b0 += 32 * 8) {
-            double w[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int b = b0 + lane + 32 * j;
-                w[j] = b < TB ? __ldcg(part + (size_t)b * 8) : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) t[0] = __dadd_rn(t[0], w[j]);
-        }
-        warp_tree<1>(t);
-        if (lane == 0) s_tot[warp] = t[0];
+        const double tot = ll_collect(ll_slot(ll_own(P), set, warp, TB, 0), TB, ep);
+        if (ORDER) fence_acq_rel(P.fence_sys);
+        if (lane == 0) s_tot[warp] = tot;
     }
     __syncthreads();
 #pragma unroll
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
         s_tab[16 + threadIdx.x] = P.inv_code[threadIdx.x];
         if (threadIdx.x < 8) s_tab[32 + threadIdx.x] = P.invA_enc[threadIdx.x];
     }
-    unsigned gen = __ldcg(P.bar_base);  // barrier target: where the previous launch left the counter
+    unsigned gen = __ldcg(P.ll_epoch);  // grid-sum epoch where the previous launch left it
     const uint32_t kc = P.cache_slots;
     DofCache<DIM, OP, TIER> cache(dyn_smem, kc);
     __syncthreads();
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
     if (PROJ) {
         double v[1] = {0.0};
         for (uint32_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], G.rhs[i]);
-        grid_sum<1>(v, 0, P, gen, s_val, s_tot);
+        grid_sum<1, false>(v, 0, P, gen, s_val, s_tot);
         mu_rhs = v[0] / P.m_global;
     }
     {
@@ -464,7 +467,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
             v[3] = __dadd_rn(v[3], zi);
             v[4] = __dadd_rn(v[4], ri);
         }
-        grid_sum_shfl<5>(v, 1, P, gen, s_warp, s_tot);
+        grid_sum_shfl<5, true>(v, 1, P, gen, s_warp, s_tot);
         if (PROJ) {
             mu = v[3] / P.m_global;
             v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
@@ -546,7 +549,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
             else
                 pass1(it == 0);
             const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            grid_sum<1>(v1, 2, P, gen, s_val, s_tot);
+            grid_sum<1, false>(v1, 2, P, gen, s_val, s_tot);
             const uint64_t t2 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             const double dq = v1[0];
             if (dq <= 0.0) { status = 2; sval = dq; sat = it; break; }
@@ -594,7 +597,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                 }
             }
             const uint64_t t3 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            grid_sum<KL>(v, 3, P, gen, s_val, s_tot);
+            grid_sum<KL, true>(v, 3, P, gen, s_val, s_tot);
             if (P.phase_ns && threadIdx.x == 0) {
                 const uint64_t t4 = gtimer();
                 ph[0] += t1 - t0;
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        *P.bar_base = gen;  // the next launch on this stream starts from here
+        *P.ll_epoch = gen;  // the next launch on this stream continues from here
         CgOut *o = P.out;
         o->iterations = its;
         o->converged = conv ? 1 : 0;

@@ -46,9 +46,11 @@ struct CgParams {
     int group_base, bpg;    // group of block b = group_base + b / bpg
     int n, nw;
     double m_global;        // DOFs summed over groups (for the mean projection)
-    double *part;           // this rank's partial buffer: 4 sets x 8 slots x total_blocks
+    double *part;           // this rank's partial buffer: 4 sets x 8 slots x total_blocks x 16 B (flag words)
     unsigned *bar;          // grid barrier counter (rank 0's on a multi-GPU run)
-    unsigned *bar_base;     // local: counter value reached by the previous launch
+    unsigned *bar_base;     // local: counter value reached by the previous launch (k_xbar)
+    unsigned *ll_epoch;     // local: grid-sum epoch reached by the previous launch
+    int fence_sys;          // ordering grid sums fence at system scope (peer memory)
     int total_blocks;       // blocks of all ranks in this solve
     int block_base;         // global index of this launch's block 0
     int npart;              // ranks whose partial buffers receive this launch's sums
