@@ -60,8 +60,8 @@ namespace {
 // ----------------------------------------------------------------- slabs
 // Vector slots of a slab.  Velocity slots have m_all[0] entries, pressure
 // slots m_all[1]; owned DOFs first, ghost-plane DOFs after.
-enum USlot { U_RHS, U_W, U_ITER, U_F, U_R, U_Z, U_D0, U_D1, U_CQ, U_TMP, U_IN, NU };
-enum PSlot { P_X, P_R, P_D, P_Z, P_Q, P_B, P_SR, P_SZ, P_SD0, P_SD1, P_SQ, P_TMP, P_IN, NP };
+enum USlot { U_RHS, U_W, U_ITER, U_F, U_R, U_Z, U_D0, U_D1, U_CQ, U_S0, U_S1, U_TMP, U_IN, NU };
+enum PSlot { P_X, P_R, P_D, P_Z, P_Q, P_B, P_SR, P_SZ, P_SD0, P_SD1, P_SQ, P_SS0, P_SS1, P_TMP, P_IN, NP };
 constexpr int FP = 3;  // family index of the pressure (velocity components are 0..dim-1)
 
 // One group of the decomposition: a slab of x-planes [x_lo, x_hi) with one
@@ -98,6 +98,7 @@ struct vs_ctx {
     uint2 *vmeta[3] = {nullptr, nullptr, nullptr};
     uint2 *pmeta = nullptr;
     uint64_t *vrec = nullptr, *prec = nullptr;
+    double2 *sdiag2 = nullptr;
     double *invS = nullptr, *d_diag_code = nullptr, *d_invA_enc = nullptr;
     std::vector<int64_t> pstart[4];  // global rank of the first DOF of plane x, x in [0, n]
     std::vector<Slab> slabs;
@@ -435,6 +436,13 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         G.d0 = op == 0 ? S.u[U_D0] : S.p[P_SD0];
         G.d1 = op == 0 ? S.u[U_D1] : S.p[P_SD1];
         G.q = op == 0 ? S.u[U_CQ] : S.p[P_SQ];
+        // k_cg1 buffers (the same slots, paired)
+        G.zb[0] = G.z;
+        G.zb[1] = G.r;
+        G.ub[0] = G.d1;
+        G.ub[1] = G.q;
+        G.sb[0] = op == 0 ? S.u[U_S0] : S.p[P_SS0];
+        G.sb[1] = op == 0 ? S.u[U_S1] : S.p[P_SS1];
         if (R > 1) {
             Slab &lo = c->slabs[(s - 1 + R) % R], &hi = c->slabs[(s + 1) % R];
             G.zpeer[0] = op == 0 ? lo.u[U_Z] : lo.p[P_SZ];
@@ -463,8 +471,6 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.part = c->part;
     P.bar = c->bar;
     P.bar_base = c->bar_base;
-    P.ll_epoch = c->bar_base + 1;
-    P.fence_sys = c->mp() ? 1 : 0;
     P.npart = c->npart;
     P.part_self = c->mp() ? c->rank : 0;
     for (int r = 0; r < c->npart; ++r) P.part_peer[r] = c->part_peer[r];
@@ -479,6 +485,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     memcpy(P.inv_code, c->inv_code, sizeof P.inv_code);
     memcpy(P.invA_enc, c->invA_enc, sizeof P.invA_enc);
     P.invS = c->invS;
+    P.sdiag2 = c->sdiag2;
     P.pf_dist = c->pf_dist;
     const CgPlan &pl = op == 0 ? c->plan_A : c->plan_S;
     P.total_blocks = pl.grid * R;          // blocks of every rank
@@ -628,7 +635,7 @@ ArenaLayout arena_layout(const Slab &S, int64_t tb_max, int R) {
     };
     for (int k = 0; k < NU; ++k) L.u[k] = take(std::max<int64_t>(1, S.m_all[0]) * sizeof(double));
     for (int k = 0; k < NP; ++k) L.p[k] = take(std::max<int64_t>(1, S.m_all[1]) * sizeof(double));
-    L.part = take((size_t)4 * 8 * tb_max * 2 * sizeof(uint64_t));  // flag-word slots (vs_cg.cu)
+    L.part = take((size_t)4 * 8 * tb_max * sizeof(double));
     L.scal = take((size_t)Q_COUNT * R * sizeof(double));
     L.bar = take(4 * sizeof(unsigned));
     L.bytes = off;
@@ -671,8 +678,24 @@ void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
         mu_max = std::max(mu_max, S.m_own[0]);
         mp_max = std::max(mp_max, S.m_own[1]);
     }
-    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device);
-    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device);
+    // one-reduction CG on a single slab; the slab decomposition keeps the
+    // two-reduction loop (its halo exchange is built for it).
+    // VOXSCHUR_CG=2 forces the two-reduction loop everywhere.
+    // It pays where the grid sums dominate (a few DOFs per thread; B200 C1
+    // 64^3: A 12.4 -> 9.7, S_hat 9.6 -> 8.5 us/it); on large solves its
+    // 18 gathers per DOF cost more than the saved sum (C2 S_hat 57.6 -> 63.3).
+    // VOXSCHUR_CG=1 / =2 forces the one- / two-reduction loop.
+    const char *ea = getenv("VOXSCHUR_CG");
+    const int force = ea ? atoi(ea) : 0;
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, C->device));
+    auto pick = [&](int64_t m) {
+        if (R > 1 || force == 2) return (int)CG_TWO_SUM;
+        if (force == 1) return (int)CG_ONE_SUM;
+        return m <= (int64_t)4 * nsm * CG_THREADS ? (int)CG_ONE_SUM : (int)CG_TWO_SUM;
+    };
+    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max));
+    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max));
     C->tb_max = (int64_t)std::max(C->plan_A.grid, C->plan_S.grid) * R;
     for (int s = C->s0; s < C->s1; ++s) {
         Slab &S = C->slabs[s];
@@ -718,8 +741,7 @@ void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
             C->bar_base = C->bar + 1;
             CK(cudaMemsetAsync(C->bar, 0, 4 * sizeof(unsigned), C->stream));
         }
-        // grid-sum slots start at epoch 0; the first sum uses epoch 1
-        CK(cudaMemsetAsync(base + L.part, 0, L.scal - L.part, C->stream));
+
     }
     C->npart = 1;
     C->part_peer[0] = C->part;
@@ -958,6 +980,7 @@ static int create_common(const uint8_t *fluid, int dim, int n, int flow_dir, int
         // diag(S_hat) by the packed face codes, summed in reference order
         const int nkey = 1 << 18;
         std::vector<double> invS(nkey, 0.0);
+        std::vector<double2> sdiag2(nkey, double2{0.0, 0.0});
         for (int key = 0; key < nkey; ++key) {
             double acc = 0.0;  // operators.py:202-206
             bool ok = true;
@@ -969,7 +992,10 @@ static int create_common(const uint8_t *fluid, int dim, int n, int flow_dir, int
             }
             const double dS = acc * C->inv_h2;
             invS[key] = (ok && dS > 0) ? 1.0 / dS : 0.0;  // krylov.py:213
+            sdiag2[key] = double2{invS[key], (ok && dS > 0) ? dS : 0.0};
         }
+        C->sdiag2 = C->alloc<double2>(nkey);
+        CK(cudaMemcpyAsync(C->sdiag2, sdiag2.data(), nkey * sizeof(double2), cudaMemcpyHostToDevice, C->stream));
         C->invS = C->alloc<double>(nkey);
         CK(cudaMemcpyAsync(C->invS, invS.data(), nkey * sizeof(double), cudaMemcpyHostToDevice, C->stream));
         C->d_diag_code = C->alloc<double>(16);

@@ -148,78 +148,48 @@ __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
-// ------------------------------------------------------- grid reductions
-// Flag-in-word ("LL") grid sums.  A block's partial is a double split into
-// two 8-byte words {epoch:32 | half:32}; an 8-byte store is single-copy
-// atomic, so a reader that sees the current epoch in both words has the
-// value -- no separate arrival counter, no release/acquire round trip just
-// to publish a scalar.  Readers poll the slots of all blocks directly.
-// Every grid sum of every launch has its own epoch (monotonic, carried
-// across launches in *P.ll_epoch), so stale slots never match.
-//
-// ORDER = the sum also orders this block's earlier global stores (z of P2,
-// the setup pass) before any reader's later loads: writers fence (release)
-// before the flag store, readers fence (acquire, which also invalidates L1)
-// after seeing the flags.  The sum after P1 needs no ordering: P2 reads only
-// d, q of its own DOFs (written by the same thread), and a block posts its
-// partial only after its P1 loads have returned (they feed the partial), so
-// P2's stores cannot race them.
-__device__ __forceinline__ void fence_acq_rel(bool sys) {
-    if (sys)
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-    else
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+// ------------------------------------------------------------- grid barrier
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void st_ll(uint64_t *p, double v, unsigned e) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-    const unsigned long long hi = (unsigned long long)e << 32;
-    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(hi | (b & 0xffffffffull)),
-                 "l"(hi | (b >> 32))
-                 : "memory");
-}
-
-// slot (set, component k, block b): two words
-__device__ __forceinline__ uint64_t *ll_slot(double *buf, int set, int k, int TB, int b) {
-    return reinterpret_cast<uint64_t *>(buf) + ((size_t)(set * 8 + k) * TB + b) * 2;
-}
-
-// Warp-wide: sum component k over all TB blocks in a fixed order (lane i:
-// blocks i, i+32, ... in chunks of 8, then an xor butterfly).  Polls until
-// every slot carries epoch e.  Result in every lane.
-__device__ __forceinline__ double ll_collect(const uint64_t *row, int TB, unsigned e) {
-    const int lane = threadIdx.x & 31;
-    double t = 0.0;
-    for (int b0 = 0; b0 < TB; b0 += 32 * 8) {
-        double w[8];
-        unsigned pend = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            w[j] = 0.0;
-            if (b0 + lane + 32 * j < TB) pend |= 1u << j;
+// (Tried: flag-in-word slots polled by every block, with no arrival
+// counter -- slower on B200: 148 blocks polling every slot costs more than
+// one counter barrier plus one read of the partials; tools/gridsum_ll.cu,
+// C1 S_hat 7.8 -> 9.5 us/it.  ORDER is accepted for that interface; the
+// counter barrier always orders.)
+// bar = monotonic arrival counter shared by every block of every rank; it is
+// never reset.  Each launch starts from *P.bar_base (the previous launch's
+// final target, written back by its block 0 -- identical on every rank, since
+// all ranks run the same barrier sequence) and each barrier adds the number
+// of participating blocks of all ranks.  One red.release per block, then
+// thread 0 polls.
+// Polling uses relaxed loads: an acquire load per poll makes ptxas emit an
+// L1 invalidation (CCTL.IVALL) per poll.  Once the target is seen, one
+// acquire re-read of the counter synchronises with every block's release
+// (the reds form one release sequence); it is 0.13 us cheaper than a
+// fence.acq_rel (B200, 148 x 1024 threads: 1.17 vs 1.30 us per barrier;
+// the unfenced floor is 0.84 us -- tools/gridsync_variants.cu).
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, unsigned total_blocks) {
+    __syncthreads();
+    target += total_blocks;
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        while ((int)(ld_relaxed(bar) - target) < 0) {
         }
-        while (pend) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (pend & (1u << j)) {
-                    unsigned long long lo, hi;
-                    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
-                                 : "=l"(lo), "=l"(hi)
-                                 : "l"(row + (size_t)(b0 + lane + 32 * j) * 2)
-                                 : "memory");
-                    if ((unsigned)(lo >> 32) == e && (unsigned)(hi >> 32) == e) {
-                        w[j] = __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
-                        pend &= ~(1u << j);
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) t = __dadd_rn(t, w[j]);
+        asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.gpu.global.u32 t, [%0];\n\t}" ::"l"(bar) : "memory");
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(~0u, t, o));
-    return t;
+    __syncthreads();
 }
 
 // Warp 0 combines the per-warp values s_warp[w][k] (w < CG_THREADS/32) with
@@ -247,26 +217,18 @@ __device__ __forceinline__ void warp_tree(double (&t)[K]) {
     }
 }
 
-// own partial buffer: one per rank (per group when ranks are emulated as groups)
-__device__ __forceinline__ double *ll_own(const CgParams &P) {
-    double *b = P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part;
-    __builtin_assume(__isGlobal(b));
-    return b;
-}
-
 // Deterministic grid-wide sum of K values over every block of every rank.
-// Block g (global index block_base + blockIdx.x) publishes its K sums into
-// slot g of partial set `set` of EVERY rank's buffer (peer stores on a
-// multi-GPU run; one buffer when the ranks are groups of one launch); every
-// block then reduces all blocks' slots of its own buffer in the same fixed
-// tree, so every block of every rank obtains bitwise-identical totals.
-// This form (K <= 5, setup only) stages the block through warp shuffles.
+// Block g (global index block_base + blockIdx.x) writes its K sums into slot
+// g of partial set `set` of EVERY rank's partial buffer (peer stores on a
+// multi-GPU run; one buffer when the ranks are groups of one launch).  After
+// the barrier each block reads all blocks' sums from its own buffer in one
+// parallel round trip and reduces them in the same fixed tree, so every
+// block of every rank obtains bitwise-identical totals.
 template <int K, bool ORDER>
-__device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgParams &P, unsigned &ep,
+__device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgParams &P, unsigned &target,
                                               double (*s_warp)[5], double *s_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int TB = P.total_blocks;
-    ++ep;
     warp_tree<K>(v);
     if (lane == 0) {
 #pragma unroll
@@ -277,35 +239,56 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
         double t[K];
         warp0_combine<K>(s_warp, t);
         if (lane < P.npart) {  // lane p stores to rank p's buffer
-            if (ORDER) fence_acq_rel(P.fence_sys);
+            double *dst = P.part_peer[lane] + (size_t)set * 8 * TB + (size_t)(P.block_base + blockIdx.x) * 8;
+            __builtin_assume(__isGlobal(dst));
 #pragma unroll
-            for (int k = 0; k < K; ++k) st_ll(ll_slot(P.part_peer[lane], set, k, TB, P.block_base + blockIdx.x), t[k], ep);
+            for (int k = 0; k < K; ++k) dst[k] = t[k];
         }
     }
-    if (warp < K) {
-        const double t = ll_collect(ll_slot(ll_own(P), set, warp, TB, 0), TB, ep);
-        if (ORDER) fence_acq_rel(P.fence_sys);
-        if (lane == 0) s_tot[warp] = t;
+    grid_barrier(P.bar, target, TB);  // starts with __syncthreads (s_warp reuse is safe)
+    // own buffer: one per rank (per group when ranks are emulated as groups)
+    const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +
+                         (size_t)set * 8 * TB;
+    __builtin_assume(__isGlobal(part));
+    double t[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) t[k] = 0.0;
+    for (int b = threadIdx.x; b < TB; b += CG_THREADS) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) t[k] = __dadd_rn(t[k], __ldcg(part + b * 8 + k));
+    }
+    warp_tree<K>(t);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) s_warp[warp][k] = t[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        warp0_combine<K>(s_warp, t);
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) s_tot[k] = t[k];
+        }
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = s_tot[k];
 }
 
-// The per-iteration form (K <= 4).  Block stage through shared memory:
+// The per-iteration form (K <= 8; s_val holds K rows).  Block stage through shared memory:
 // every thread stores its K values, then warp k alone reduces component k
 // -- lane i sums threads i, i+32, ..., i+992 in a fixed pairwise tree, one
 // xor butterfly combines the lanes.  The shuffle tree over all 32 warps
 // cost 32 x K x 10 SHFL per block and was SHFL-throughput bound (B200,
-// tools/gridsum_variants.cu).  Warp k then publishes component k and
-// collects it over the blocks.
+// tools/gridsum_variants.cu: K=4 3.93 -> 2.77 us, K=2 2.95 -> 2.52 us per
+// grid sum).  After the barrier warp k again reduces component k over the
+// blocks (lane i: blocks i, i+32, ... in order; loads issued 8 at a time).
 template <int K, bool ORDER>
-__device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams &P, unsigned &ep,
+__device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams &P, unsigned &target,
                                          double (*s_val)[CG_THREADS], double *s_tot) {
-    static_assert(K >= 1 && K <= 4, "grid_sum stages at most 4 components");
+    static_assert(K >= 1 && K <= 8, "grid_sum stages at most 8 components");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int TB = P.total_blocks;
-    ++ep;
 #pragma unroll
     for (int k = 0; k < K; ++k) s_val[k][threadIdx.x] = v[k];
     __syncthreads();
@@ -333,12 +316,31 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
             t[0] = __dadd_rn(c[0], c[1]);
         warp_tree<1>(t);
         if (lane < P.npart) {  // lane p stores to rank p's buffer
-            if (ORDER) fence_acq_rel(P.fence_sys);
-            st_ll(ll_slot(P.part_peer[lane], set, warp, TB, P.block_base + blockIdx.x), t[0], ep);
+            double *dst =
+                P.part_peer[lane] + (size_t)set * 8 * TB + (size_t)(P.block_base + blockIdx.x) * 8 + warp;
+            __builtin_assume(__isGlobal(dst));
+            *dst = t[0];
         }
-        const double tot = ll_collect(ll_slot(ll_own(P), set, warp, TB, 0), TB, ep);
-        if (ORDER) fence_acq_rel(P.fence_sys);
-        if (lane == 0) s_tot[warp] = tot;
+    }
+    grid_barrier(P.bar, target, TB);  // starts with __syncthreads (s_val reuse is safe)
+    if (warp < K) {
+        // own buffer: one per rank (per group when ranks are emulated as groups)
+        const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +
+                             (size_t)set * 8 * TB + warp;
+        __builtin_assume(__isGlobal(part));
+        double t[1] = {0.0};
+        for (int b0 = 0; b0 < TB; b0 += 32 * 8) {
+            double w[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int b = b0 + lane + 32 * j;
+                w[j] = b < TB ? __ldcg(part + (size_t)b * 8) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) t[0] = __dadd_rn(t[0], w[j]);
+        }
+        warp_tree<1>(t);
+        if (lane == 0) s_tot[warp] = t[0];
     }
     __syncthreads();
 #pragma unroll
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
         s_tab[16 + threadIdx.x] = P.inv_code[threadIdx.x];
         if (threadIdx.x < 8) s_tab[32 + threadIdx.x] = P.invA_enc[threadIdx.x];
     }
-    unsigned gen = __ldcg(P.ll_epoch);  // grid-sum epoch where the previous launch left it
+    unsigned gen = __ldcg(P.bar_base);  // barrier target: where the previous launch left the counter
     const uint32_t kc = P.cache_slots;
     DofCache<DIM, OP, TIER> cache(dyn_smem, kc);
     __syncthreads();
@@ -630,7 +632,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        *P.ll_epoch = gen;  // the next launch on this stream continues from here
+        *P.bar_base = gen;  // the next launch on this stream starts from here
         CgOut *o = P.out;
         o->iterations = its;
         o->converged = conv ? 1 : 0;
@@ -644,32 +646,316 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
     }
 }
 
+// ===================================================================
+// k_cg1 -- the same Jacobi-PCG with ONE grid reduction per iteration
+// (Chronopoulos-Gear form of krylov.py:76-182, M-scaled recurrences).
+//
+// The two-reduction loop above keeps the reference's exact elementwise
+// operation order but pays two grid-wide sums per iteration (~2.5-4 us each
+// on B200, tools/gridsum_ll.cu), which dominates small solves.  With
+//   zr = M r (unprojected), z = zr - mu, w = A zr, u = M w, s = M q,
+//   gamma = r.z, delta = z.w,
+// the recurrences (exact arithmetic identical to the reference's CG)
+//   beta_i  = gamma_i / gamma_{i-1},  alpha_i = gamma_i / (delta_i - beta_i gamma_i / alpha_{i-1})
+//   d_i = z_i + beta_i d_{i-1},  s_i = u_i + beta_i s_{i-1}
+//   x_{i+1} = x_i - alpha_i d_i,  zr_{i+1} = zr_i - alpha_i s_i
+//   w_{i+1} = A zr_{i+1},  u_{i+1} = M w_{i+1}
+// need the sums gamma_{i+1}, delta_{i+1}, |z_{i+1}| only after the pass
+// that produces zr_{i+1}: one pass, one reduction.  A neighbour's zr_{i+1}
+// is recomputed from its zr_i, u_i, s_{i-1} (no second pass; M of the
+// neighbour is never needed because u and s are stored M-scaled).  For the
+// projected S_hat solve, A annihilates constants, so w = A zr = A z and
+// delta = zr.w - mu sum w; r = zr * diag(S_hat).
+// zr, u, s are double-buffered (neighbours read the old values while the
+// pass writes the new); x and d are per-DOF and updated in place.
+// DRAM bytes per DOF per iteration: read x, d, zr, u, s; write x, d, zr,
+// u, s -> 80 B (+ the record when not smem-cached).
+// Parity: values and iteration counts agree with the reference's
+// two-reduction form to rounding (tests/test_gpu_scale.py: counts within
+// 2 %, solutions within 1e-8); elementwise order is no longer bitwise.
+// k_cg1 grid-sum staging in dynamic smem (KS rows of CG_THREADS doubles)
+__host__ __device__ constexpr size_t cg1_stage_bytes(int op) { return (size_t)(op == 1 ? 6 : 3) * CG_THREADS * 8; }
+
+template <int OP>
+__device__ __forceinline__ void inv_diag(uint64_t rc, const Tabs &T, const double2 *__restrict__ sdg, double &inv,
+                                         double &dg) {
+    if (OP == 0) {
+        inv = T.inv[rec_vcode(rc)];
+        dg = T.diag[rec_vcode(rc)];
+    } else {
+        const double2 t = __ldg(sdg + rec_pkey(rc));
+        inv = t.x;
+        dg = t.y;
+    }
+}
+
+template <int DIM, int OP, int TIER>
+__global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
+    constexpr bool PROJ = (OP == 1);
+    constexpr int NS = 2 * DIM;
+    constexpr int KS = PROJ ? 6 : 3;  // per-iteration sums
+    extern __shared__ __align__(16) uint8_t dyn_smem[];
+    __shared__ double s_tab[40];
+    __shared__ double s_warp[CG_THREADS / 32][5];
+    __shared__ double s_tot[8];
+    __shared__ CgGroup G;
+    // dynamic smem: [grid-sum staging KS x CG_THREADS doubles | DOF cache]
+    double(*s_val)[CG_THREADS] = reinterpret_cast<double(*)[CG_THREADS]>(dyn_smem);
+    if (threadIdx.x == 0) G = P.groups[P.group_base + blockIdx.x / P.bpg];
+    if (threadIdx.x < 16) {
+        s_tab[threadIdx.x] = P.diag_code[threadIdx.x];
+        s_tab[16 + threadIdx.x] = P.inv_code[threadIdx.x];
+        if (threadIdx.x < 8) s_tab[32 + threadIdx.x] = P.invA_enc[threadIdx.x];
+    }
+    unsigned ep = __ldcg(P.bar_base);
+    const uint32_t kc = P.cache_slots;
+    DofCache<DIM, OP, TIER> cache(dyn_smem + cg1_stage_bytes(OP), kc);
+    __syncthreads();
+    const Tabs T{s_tab, s_tab + 16, s_tab + 32, P.invS};
+    const double2 *sdg = P.sdiag2;
+    const uint32_t m = G.m_own;
+    const uint32_t tid = (blockIdx.x % P.bpg) * CG_THREADS + threadIdx.x;
+    const uint32_t stride = P.bpg * CG_THREADS;
+    double *x = G.x, *dv = G.d0;
+    __builtin_assume(__isGlobal(x));
+    __builtin_assume(__isGlobal(dv));
+    const double inv_h = P.inv_h, inv_h2 = P.inv_h2;
+    int cur = 0;  // zb/ub/sb[cur] hold zr_i, u_i, s_{i-1}
+    auto buf = [&](double *const(&b)[2], int k) -> double * {
+        double *p = b[k];
+        __builtin_assume(__isGlobal(p));
+        return p;
+    };
+
+    // ---- setup 1 (krylov.py:102-119): project rhs; r0 = op(x0) - rhs;
+    //      zr0 = M r0; fill the DOF cache
+    double mu_rhs = 0.0;
+    if (PROJ) {
+        double v[1] = {0.0};
+        for (uint32_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], G.rhs[i]);
+        grid_sum<1, false>(v, 0, P, ep, s_val, s_tot);
+        mu_rhs = v[0] / P.m_global;
+    }
+    double mu, gamma, rp0, ru0;
+    {
+        double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        const double *x0 = G.x0;
+        double *zr = buf(G.zb, 0);
+        uint32_t k = 0;
+        for (uint32_t i = tid; i < m; i += stride, ++k) {
+            const uint64_t rc = G.rec[i];
+            uint32_t nr[NS];
+            if (x0 || (TIER == 2 && k < kc))
+                neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, i, nr);
+            if (k < kc) cache.put(k, rc, nr);
+            double ax = 0.0, xi = 0.0;
+            if (x0) {
+                xi = x0[i];
+                double vn[NS];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) vn[s] = nr[s] != ABSENT ? x0[nr[s]] : 0.0;
+                ax = op_value<DIM, OP>(rc, xi, vn, T, inv_h, inv_h2);
+            }
+            x[i] = xi;
+            const double b = PROJ ? __dsub_rn(G.rhs[i], mu_rhs) : G.rhs[i];
+            const double ri = __dsub_rn(ax, b);
+            double inv, dg;
+            inv_diag<OP>(rc, T, sdg, inv, dg);
+            const double zi = __dmul_rn(ri, inv);
+            zr[i] = zi;
+            v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
+            v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
+            v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
+            v[3] = __dadd_rn(v[3], zi);
+            v[4] = __dadd_rn(v[4], ri);
+        }
+        grid_sum_shfl<5, true>(v, 1, P, ep, s_warp, s_tot);
+        mu = PROJ ? v[3] / P.m_global : 0.0;
+        gamma = PROJ ? __dsub_rn(v[0], __dmul_rn(mu, v[4])) : v[0];
+        rp0 = sqrt(PROJ ? __dsub_rn(v[1], __dmul_rn(mu, v[3])) : v[1]);
+        ru0 = sqrt(v[2]);
+    }
+    // ---- setup 2: w0 = A zr0, u0 = M w0; delta0 = z0.w0
+    double delta;
+    {
+        double v[2] = {0.0, 0.0};
+        const double *zr = buf(G.zb, 0);
+        double *u = buf(G.ub, 0);
+        uint32_t k = 0;
+        for (uint32_t i = tid; i < m; i += stride, ++k) {
+            uint64_t rc;
+            uint32_t nr[NS];
+            fetch_dof<DIM, OP, TIER>(P, G, cache, k, kc, i, rc, nr);
+            const double zi = zr[i];
+            double vn[NS];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                const uint32_t j = nr[s] != ABSENT ? nr[s] : i;
+                const double zj = zr[j];
+                vn[s] = (OP == 0 && nr[s] == ABSENT) ? 0.0 : zj;
+            }
+            const double w = op_value<DIM, OP>(rc, zi, vn, T, inv_h, inv_h2);
+            double inv, dg;
+            inv_diag<OP>(rc, T, sdg, inv, dg);
+            u[i] = __dmul_rn(w, inv);
+            v[0] = __dadd_rn(v[0], __dmul_rn(zi, w));
+            v[1] = __dadd_rn(v[1], w);
+        }
+        grid_sum<2, true>(v, 2, P, ep, s_val, s_tot);
+        delta = PROJ ? __dsub_rn(v[0], __dmul_rn(mu, v[1])) : v[0];
+    }
+    const double ref = rp0;
+    double gamma_prev = 0.0, alpha_prev = 0.0, rp_last = rp0, sval = 0.0;
+    int status = 0;
+    int64_t sat = 0, its = 0;
+    bool conv = (ref == 0.0);
+    unsigned long long ph[4] = {0, 0, 0, 0};
+    if (!conv) {
+        for (int64_t it = 0; it < P.max_iter; ++it) {
+            if (gamma < 0.0) { status = 1; sval = gamma; sat = it; break; }
+            if (gamma == 0.0) { conv = true; break; }
+            double beta, dq;
+            if (it == 0) {
+                beta = 0.0;
+                dq = delta;
+            } else {
+                beta = gamma / gamma_prev;
+                dq = __dsub_rn(delta, __dmul_rn(beta, gamma) / alpha_prev);
+            }
+            if (dq <= 0.0) { status = 2; sval = dq; sat = it; break; }
+            const double alpha = gamma / dq;
+            const uint64_t t0 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
+            double v[KS];
+#pragma unroll
+            for (int q = 0; q < KS; ++q) v[q] = 0.0;
+            auto pass = [&](auto first_c) {
+                constexpr bool first = decltype(first_c)::value;
+                const double *zr = buf(G.zb, cur), *u = buf(G.ub, cur), *so = buf(G.sb, cur);
+                double *zn_o = buf(G.zb, cur ^ 1), *un_o = buf(G.ub, cur ^ 1), *sn_o = buf(G.sb, cur ^ 1);
+                uint32_t k = 0;
+                for (uint32_t i = tid; i < m; i += stride, ++k) {
+                    uint64_t rc;
+                    uint32_t nr[NS];
+                    fetch_dof<DIM, OP, TIER>(P, G, cache, k, kc, i, rc, nr);
+                    const double zc = zr[i], uc = u[i], xc = x[i];
+                    const double sc = first ? 0.0 : so[i], dc = first ? 0.0 : dv[i];
+                    double vn[NS];
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) {  // unconditional loads (absent -> own index)
+                        const uint32_t j = nr[s] != ABSENT ? nr[s] : i;
+                        const double zj = zr[j], uj = u[j];
+                        const double sj = first ? uj : __dadd_rn(uj, __dmul_rn(beta, so[j]));
+                        const double zn = __dsub_rn(zj, __dmul_rn(alpha, sj));
+                        vn[s] = (OP == 0 && nr[s] == ABSENT) ? 0.0 : zn;
+                    }
+                    const double z0 = PROJ ? __dsub_rn(zc, mu) : zc;
+                    const double di = first ? z0 : __dadd_rn(z0, __dmul_rn(beta, dc));
+                    const double si = first ? uc : __dadd_rn(uc, __dmul_rn(beta, sc));
+                    const double zi = __dsub_rn(zc, __dmul_rn(alpha, si));
+                    const double w = op_value<DIM, OP>(rc, zi, vn, T, inv_h, inv_h2);
+                    double inv, dg;
+                    inv_diag<OP>(rc, T, sdg, inv, dg);
+                    x[i] = __dsub_rn(xc, __dmul_rn(alpha, di));
+                    dv[i] = di;
+                    sn_o[i] = si;
+                    zn_o[i] = zi;
+                    un_o[i] = __dmul_rn(w, inv);
+                    const double ri = __dmul_rn(zi, dg);
+                    v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
+                    v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
+                    v[2] = __dadd_rn(v[2], __dmul_rn(zi, w));
+                    if (PROJ) {
+                        v[3] = __dadd_rn(v[3], zi);
+                        v[4] = __dadd_rn(v[4], ri);
+                        v[5] = __dadd_rn(v[5], w);
+                    }
+                }
+            };
+            if (it == 0)
+                pass(std::true_type{});
+            else
+                pass(std::false_type{});
+            const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
+            grid_sum<KS, true>(v, 3, P, ep, s_val, s_tot);
+            if (P.phase_ns && threadIdx.x == 0) {
+                const uint64_t t2 = gtimer();
+                ph[0] += t1 - t0;
+                ph[1] += t2 - t1;
+            }
+            gamma_prev = gamma;
+            alpha_prev = alpha;
+            cur ^= 1;
+            double nz2;
+            if (PROJ) {
+                mu = v[3] / P.m_global;
+                gamma = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
+                nz2 = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
+                delta = __dsub_rn(v[2], __dmul_rn(mu, v[5]));
+            } else {
+                gamma = v[0];
+                nz2 = v[1];
+                delta = v[2];
+            }
+            const double nz = sqrt(nz2);
+            if (!isfinite(nz)) { status = 3; sat = it + 1; break; }
+            its = it + 1;
+            rp_last = nz;
+            if (nz / ref < P.tol) { conv = true; break; }
+        }
+    }
+    if (P.phase_ns && threadIdx.x == 0) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            if (blockIdx.x == 0) P.phase_ns[p] += ph[p];
+            atomicMax(P.phase_ns + 4 + p, ph[p]);
+            atomicAdd(P.phase_ns + 8 + p, ph[p]);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *P.bar_base = ep;
+        CgOut *o = P.out;
+        o->iterations = its;
+        o->converged = conv ? 1 : 0;
+        o->status = status;
+        o->value = sval;
+        o->at_iter = sat;
+        o->res_prec0 = rp0;
+        o->res_unprec0 = ru0;
+        o->res_prec_last = rp_last;
+        o->res_unprec_last = ru0;
+    }
+}
+
 template <int DIM, int OP>
-static const void *pcg_fn_t(int tier) {
+static const void *pcg_fn_t(int tier, int alg) {
+    if (alg == CG_ONE_SUM) return tier == 2 ? (const void *)k_cg1<DIM, OP, 2> : (const void *)k_cg1<DIM, OP, 1>;
     return tier == 2 ? (const void *)k_pcg<DIM, OP, 2> : (const void *)k_pcg<DIM, OP, 1>;
 }
-static const void *pcg_fn(int dim, int op, int tier) {
-    if (dim == 3) return op == 0 ? pcg_fn_t<3, 0>(tier) : pcg_fn_t<3, 1>(tier);
-    return op == 0 ? pcg_fn_t<2, 0>(tier) : pcg_fn_t<2, 1>(tier);
+static const void *pcg_fn(int dim, int op, int tier, int alg) {
+    if (dim == 3) return op == 0 ? pcg_fn_t<3, 0>(tier, alg) : pcg_fn_t<3, 1>(tier, alg);
+    return op == 0 ? pcg_fn_t<2, 0>(tier, alg) : pcg_fn_t<2, 1>(tier, alg);
 }
 
 // Plan one launch: blocks per group (all groups co-resident on one device),
 // cache tier and slots, smem.  m = the largest owned DOF count of a group.
-CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device) {
+CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg) {
     CgPlan pl{};
+    pl.alg = alg;
     int nsm = 0, maxopt = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     const int ns = 2 * dim;
     for (int tier = 2; tier >= 1; --tier) {
-        const void *fn = pcg_fn(dim, op, tier);
+        const void *fn = pcg_fn(dim, op, tier, alg);
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, fn);  // static smem (grid_sum staging, tables)
-        size_t budget = std::min<size_t>(CG_SMEM_BUDGET, (size_t)maxopt - fa.sharedSizeBytes);
-        if (const char *e = getenv("VOXSCHUR_SMEM_KB")) budget = std::min<size_t>(budget, (size_t)atoi(e) * 1024);
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
+        const size_t stage = alg == CG_ONE_SUM ? cg1_stage_bytes(op) : 0;  // dynamic grid-sum staging
+        size_t total = std::min<size_t>(CG_SMEM_BUDGET + stage, (size_t)maxopt - fa.sharedSizeBytes);
+        if (const char *e = getenv("VOXSCHUR_SMEM_KB")) total = std::min<size_t>(total, (size_t)atoi(e) * 1024 + stage);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)total);
+        const size_t budget = total - stage;  // DOF cache
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CG_THREADS, budget);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CG_THREADS, total);
         if (per_sm < 1) per_sm = 1;
         int grid = (int)std::max<int64_t>(
             1, std::min<int64_t>((int64_t)per_sm * nsm / groups, (m + CG_THREADS - 1) / CG_THREADS));
@@ -680,7 +966,7 @@ CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device) {
         pl.tier = tier;
         pl.grid = grid;
         pl.slots = (uint32_t)std::min<int64_t>(slots, (int64_t)(budget / per_slot));
-        pl.smem = pl.slots * per_slot;
+        pl.smem = stage + pl.slots * per_slot;
         return pl;
     }
     return pl;
@@ -691,7 +977,7 @@ cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &
     P.cache_slots = pl.slots;
     P.bpg = pl.grid;
     void *args[] = {&P};
-    return cudaLaunchCooperativeKernel(pcg_fn(dim, op, pl.tier), dim3(pl.grid * groups), dim3(CG_THREADS), args,
+    return cudaLaunchCooperativeKernel(pcg_fn(dim, op, pl.tier, pl.alg), dim3(pl.grid * groups), dim3(CG_THREADS), args,
                                        pl.smem, s);
 }
 

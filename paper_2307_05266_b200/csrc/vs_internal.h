@@ -34,6 +34,7 @@ struct CgGroup {
     uint32_t m_own, m_all;  // owned DOFs, owned + ghost
     const double *rhs, *x0;
     double *x, *r, *z, *d0, *d1, *q;
+    double *zb[2], *ub[2], *sb[2];  // k_cg1: double-buffered zr = M r, u = M A zr, s = M q
     // halo: side s = 0 sends the first owned plane to the lower neighbour's
     // ghost_hi, s = 1 the last owned plane to the upper neighbour's ghost_lo;
     // per family f, local range [sbeg, send) -> zpeer[s][sdst + (i - sbeg)]
@@ -46,11 +47,9 @@ struct CgParams {
     int group_base, bpg;    // group of block b = group_base + b / bpg
     int n, nw;
     double m_global;        // DOFs summed over groups (for the mean projection)
-    double *part;           // this rank's partial buffer: 4 sets x 8 slots x total_blocks x 16 B (flag words)
+    double *part;           // this rank's partial buffer: 4 sets x 8 slots x total_blocks
     unsigned *bar;          // grid barrier counter (rank 0's on a multi-GPU run)
-    unsigned *bar_base;     // local: counter value reached by the previous launch (k_xbar)
-    unsigned *ll_epoch;     // local: grid-sum epoch reached by the previous launch
-    int fence_sys;          // ordering grid sums fence at system scope (peer memory)
+    unsigned *bar_base;     // local: counter value reached by the previous launch
     int total_blocks;       // blocks of all ranks in this solve
     int block_base;         // global index of this launch's block 0
     int npart;              // ranks whose partial buffers receive this launch's sums
@@ -65,6 +64,7 @@ struct CgParams {
     double inv_code[16];
     double invA_enc[8];
     const double *invS;
+    const double2 *sdiag2;         // S_hat {1/diag, diag} by 18-bit key (k_cg1)
     uint32_t cache_slots;
     uint32_t pf_dist;              // L2 prefetch distance in grid strides (0 = off)
     unsigned long long *phase_ns;  // optional [12] accumulators
@@ -113,12 +113,14 @@ void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64
 int launch_reduce(int kind, const double *a, const double *b, int64_t m, double *part, double *out,
                   cudaStream_t s);
 constexpr size_t CG_SMEM_BUDGET = 200 * 1024;  // dynamic smem per block (1 block / SM)
+enum CgAlg { CG_TWO_SUM = 0, CG_ONE_SUM = 1 };  // k_pcg (reference order) | k_cg1 (one reduction)
 struct CgPlan {
+    int alg;
     int tier, grid;
     uint32_t slots;
     size_t smem;
 };
-CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device);
+CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg);
 cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
 
 }  // namespace vs
