@@ -118,6 +118,8 @@ struct vs_ctx {
     double *h_scal = nullptr;  // pinned
     CgOut *h_cg = nullptr;     // pinned
     CgPlan plan_A{}, plan_S{};
+    TilePlan tile_A{}, tile_S{};  // k_cg1t plans (one slab, 3D); used when use_tile[op]
+    bool use_tile[2] = {false, false};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
     vs_kstat st_A{}, st_S{};  // stats of the last top-level call
     int64_t launches = 0;
@@ -140,6 +142,8 @@ struct vs_ctx {
     }
     ~vs_ctx() {
         if (device >= 0) cudaSetDevice(device);
+        if (tile_A.mem) cudaFree(tile_A.mem);
+        if (tile_S.mem) cudaFree(tile_S.mem);
         for (void *p : allocs) cudaFree(p);
         if (h_scal) cudaFreeHost(h_scal);
         if (h_cg) cudaFreeHost(h_cg);
@@ -496,7 +500,14 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         c->evpool.push_back(e);
     }
     CK(cudaEventRecord(c->evpool[2 * li], c->stream));
-    CK(launch_pcg(c->dim, op, pl, nloc, P, c->stream));
+    if (c->use_tile[op]) {
+        const TilePlan &tp = op == 0 ? c->tile_A : c->tile_S;
+        P.total_blocks = tp.grid;
+        P.block_base = 0;
+        CK(launch_cg1t(op, tp, P, c->stream));
+    } else {
+        CK(launch_pcg(c->dim, op, pl, nloc, P, c->stream));
+    }
     CK(cudaEventRecord(c->evpool[2 * li + 1], c->stream));
     ++c->launches;
     return li;
@@ -696,6 +707,19 @@ void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
     };
     C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max));
     C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max));
+    // plane-sweep TMA tiles (k_cg1t): VOXSCHUR_TILED=1 turns them on
+    const char *et = getenv("VOXSCHUR_TILED");
+    if (et && atoi(et) == 1 && dim == 3 && R == 1 && !(C->nw & 1)) {
+        const uint2 *mA[3] = {C->vmeta[0], C->vmeta[1], C->vmeta[2]};
+        const int64_t fA[3] = {C->vcount[0], C->vcount[1], C->vcount[2]};
+        C->tile_A = tile_plan(0, n, C->nw, 3, mA, fA, C->device, C->stream);
+        const uint2 *mS[1] = {C->pmeta};
+        const int64_t fS[1] = {C->m_p};
+        C->tile_S = tile_plan(1, n, C->nw, 1, mS, fS, C->device, C->stream);
+        C->use_tile[0] = C->tile_A.ok;
+        C->use_tile[1] = C->tile_S.ok;
+        CK(cudaGetLastError());
+    }
     C->tb_max = (int64_t)std::max(C->plan_A.grid, C->plan_S.grid) * R;
     for (int s = C->s0; s < C->s1; ++s) {
         Slab &S = C->slabs[s];

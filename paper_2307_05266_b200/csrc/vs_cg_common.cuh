@@ -174,9 +174,9 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, un
 // Warp 0 combines the per-warp values s_warp[w][k] (w < CG_THREADS/32) with
 // one xor-butterfly carrying all K values at once; the result lands in
 // every lane of warp 0.  Fixed shape -> bitwise identical in every block.
-template <int K>
+template <int K, int NT = CG_THREADS>
 __device__ __forceinline__ void warp0_combine(const double (*s_warp)[5], double (&t)[K]) {
-    constexpr int NW = CG_THREADS / 32;
+    constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 0; k < K; ++k) t[k] = lane < NW ? s_warp[lane][k] : 0.0;
@@ -203,7 +203,7 @@ __device__ __forceinline__ void warp_tree(double (&t)[K]) {
 // the barrier each block reads all blocks' sums from its own buffer in one
 // parallel round trip and reduces them in the same fixed tree, so every
 // block of every rank obtains bitwise-identical totals.
-template <int K, bool ORDER>
+template <int K, bool ORDER, int NT = CG_THREADS>
 __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgParams &P, unsigned &target,
                                               double (*s_warp)[5], double *s_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -216,7 +216,7 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
     __syncthreads();
     if (warp == 0) {
         double t[K];
-        warp0_combine<K>(s_warp, t);
+        warp0_combine<K, NT>(s_warp, t);
         if (lane < P.npart) {  // lane p stores to rank p's buffer
             double *dst = P.part_peer[lane] + (size_t)set * 8 * TB + (size_t)(P.block_base + blockIdx.x) * 8;
             __builtin_assume(__isGlobal(dst));
@@ -232,7 +232,7 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
     double t[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) t[k] = 0.0;
-    for (int b = threadIdx.x; b < TB; b += CG_THREADS) {
+    for (int b = threadIdx.x; b < TB; b += NT) {
 #pragma unroll
         for (int k = 0; k < K; ++k) t[k] = __dadd_rn(t[k], __ldcg(part + b * 8 + k));
     }
@@ -243,7 +243,7 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
     }
     __syncthreads();
     if (warp == 0) {
-        warp0_combine<K>(s_warp, t);
+        warp0_combine<K, NT>(s_warp, t);
         if (lane == 0) {
 #pragma unroll
             for (int k = 0; k < K; ++k) s_tot[k] = t[k];
@@ -262,9 +262,9 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
 // tools/gridsum_variants.cu: K=4 3.93 -> 2.77 us, K=2 2.95 -> 2.52 us per
 // grid sum).  After the barrier warp k again reduces component k over the
 // blocks (lane i: blocks i, i+32, ... in order; loads issued 8 at a time).
-template <int K, bool ORDER>
+template <int K, bool ORDER, int NT = CG_THREADS>
 __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams &P, unsigned &target,
-                                         double (*s_val)[CG_THREADS], double *s_tot) {
+                                         double (*s_val)[NT], double *s_tot) {
     static_assert(K >= 1 && K <= 8, "grid_sum stages at most 8 components");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int TB = P.total_blocks;
@@ -273,7 +273,7 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
     __syncthreads();
     if (warp < K) {
         // chunks of 8 (pairwise within a chunk), then the chunk sums pairwise
-        constexpr int NC = CG_THREADS / 256;
+        constexpr int NC = NT / 256;
         static_assert(NC == 2 || NC == 4, "grid_sum block stage: 512 or 1024 threads");
         double c[NC];
 #pragma unroll

@@ -123,4 +123,51 @@ struct CgPlan {
 CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg);
 cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
 
+// ---- k_cg1t: plane-sweep tiles staged by TMA (vs_cgt.cu) ----------------
+// A unit = one DOF family (velocity component / pressure), a run of own
+// lines [ya, ya + H) of every plane in [x0, x1]; the block sweeps its
+// planes in x with the window (own lines +- 1 line) of planes x-1, x, x+1
+// resident in shared memory.
+struct TileUnit {
+    int32_t fam;     // family: velocity component (A) or 0 (S_hat)
+    int32_t ya;      // first own line
+    int32_t wrap;    // 1: the window is the whole plane (y neighbours wrap inside it)
+    int32_t nwl;     // window lines
+    int32_t npc;     // window pieces (contiguous rank runs): 1 or 2
+    int32_t pwl1;    // first window line of piece 1
+    int32_t nplanes; // descriptors: halo plane, compute planes, halo plane
+    uint32_t desc0;  // index of the first descriptor
+};
+struct PlaneDesc {               // 48 B (a multiple of 16: bulk-copied), one per plane of a unit
+    uint32_t own_start, own_len; // own DOFs (ranks) of the plane
+    uint32_t vstart[2], vlen[2]; // window pieces in doubles (even start and length)
+    uint32_t mstart[2], mlen[2]; // window pieces in meta words (even start and length)
+    uint32_t pad[2];
+};
+static_assert(sizeof(PlaneDesc) % 16 == 0, "PlaneDesc is bulk-copied");
+struct TileParams {
+    const TileUnit *units;
+    const uint32_t *blk_unit;  // block b runs units [blk_unit[b], blk_unit[b + 1])
+    const PlaneDesc *planes;
+    uint32_t capg;             // window capacity per slot and vector (doubles, even)
+    uint32_t capo;             // own-slice capacity per slot and stream (8-B words, even)
+    uint32_t capm;             // meta words per slot (even)
+    uint32_t wlmax;            // window lines (max)
+    uint32_t dmax;             // descriptors per unit (max)
+};
+struct TilePlan {
+    bool ok = false;
+    int grid = 0;
+    size_t smem = 0;
+    int H[3] = {0, 0, 0};
+    int64_t units = 0;
+    TileParams tp{};
+    void *mem = nullptr;       // device copy of units, blk_unit, planes
+};
+// Plan the tiles of one operator's families on `device` (meta/m per family,
+// one slab, 3D, nw even).  Returns ok = false when the shapes do not fit.
+TilePlan tile_plan(int op, int n, int nw, int nfam, const uint2 *const *meta, const int64_t *m_fam, int device,
+                   cudaStream_t s);
+cudaError_t launch_cg1t(int op, const TilePlan &tp, CgParams &P, cudaStream_t s);
+
 }  // namespace vs
