@@ -162,6 +162,10 @@ typedef struct {
     int64_t iterations;   /* CG iterations summed over those launches   */
     int64_t dof_iters;    /* iterations x DOFs summed over launches     */
     double ms;            /* summed CUDA-event duration of the launches */
+    int32_t kernel;       /* which fused CG ran: 0 k_pcg (two grid sums per
+                             iteration, reference operation order), 1 k_cg1
+                             (one grid sum), 2 k_cg1t (one grid sum, tiled) */
+    int32_t reserved;
 } vs_kstat;
 
 int vs_kernel_stats(vs_ctx *ctx, vs_kstat *velocity_cg, vs_kstat *simple_cg,

@@ -50,6 +50,8 @@ class VsKstat(C.Structure):
         ("iterations", C.c_int64),
         ("dof_iters", C.c_int64),
         ("ms", C.c_double),
+        ("kernel", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

@@ -529,6 +529,7 @@ void drain_log(vs_ctx *c, int from, int64_t *its_op) {
         st.iterations += o.iterations;
         st.dof_iters += o.iterations * m;
         st.ms += ms;
+        st.kernel = c->use_tile[op] ? 2 : (op == 0 ? c->plan_A.alg : c->plan_S.alg);
         if (its_op) its_op[li - from] = o.iterations;
         if (m) {
             Status s = cg_status_to_error(o, op);

@@ -498,7 +498,10 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
             else
                 pass(std::false_type{});
             const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            grid_sum<KS, true>(v, 3, P, ep, s_val, s_tot);
+            // consecutive grid sums must use different partial sets: a block that
+            // is one pass ahead writes the next sum while a slow block may still
+            // read this one (same set -> diverging scalars -> barrier deadlock)
+            grid_sum<KS, true>(v, 3 - (int)(it & 1), P, ep, s_val, s_tot);
             if (P.phase_ns && threadIdx.x == 0) {
                 const uint64_t t2 = gtimer();
                 ph[0] += t1 - t0;

@@ -449,7 +449,8 @@ __global__ void __launch_bounds__(TT, 1) k_cg1t(const CgParams P, const TilePara
             }
             __syncthreads();  // the ring is idle: the grid sum stages through it
             const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            grid_sum<KS, true, TT>(v, 3, P, gen, s_val, s_tot);
+            // alternate partial sets (see k_cg1): consecutive sums never share one
+            grid_sum<KS, true, TT>(v, 3 - (int)(it & 1), P, gen, s_val, s_tot);
             if (P.phase_ns && threadIdx.x == 0) {
                 const uint64_t t2 = gtimer();
                 phn[0] += t1 - t0;
