@@ -77,6 +77,30 @@ def test_c1_capped_solve_vs_oracle(c1, prec):
         assert within_2pct(rep.inner_iter_totals[key], orc["inner_iter_totals"][key])
 
 
+@pytest.mark.parametrize("env", [{"VOXSCHUR_CG": "2"}, {"VOXSCHUR_TILED": "1"}])
+def test_c1_other_kernels_vs_oracle(c1, monkeypatch, env):
+    """The C1 inner solves with the two-reduction k_pcg (forced) and with the
+    experimental TMA-staged plane sweep k_cg1t, against the oracle."""
+    grid, _, o = c1
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    s = vx.assemble(grid, 0)
+    want = "k_pcg" if "VOXSCHUR_CG" in env else "k_cg1t"
+    rng = np.random.default_rng(5)
+    p = rng.standard_normal(s.m_p)
+    p -= p.mean()
+    rhs = o.apply_gradient(p)
+    x, its = schur._solve_velocity(s, rhs, 1e-12)
+    xo, io = vo.solve_velocity(o, rhs, 1e-12)
+    assert vx.last_kernel_stats(s)["velocity_cg"]["kernel"] == want
+    assert within_2pct(its, io) and rel_err(x, xo) < REL
+    z = vx.apply_simple_inverse(s, p, 1e-12)
+    zo, io = vo.solve_simple(o, p, 1e-12)
+    st = vx.last_kernel_stats(s)["simple_cg"]
+    assert st["kernel"] == want and within_2pct(st["iterations"], io)
+    assert rel_err(z, zo) < REL
+
+
 def test_c1_slabs_match_single(c1):
     grid, s, _ = c1
     s4 = vx.assemble(grid, 0, slabs=4)
