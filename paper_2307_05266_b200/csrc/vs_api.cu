@@ -77,6 +77,7 @@ struct Slab {
     int64_t m_own[2] = {0, 0}, m_all[2] = {0, 0};
     uint2 *meta[4] = {nullptr, nullptr, nullptr, nullptr};
     uint64_t *vrec = nullptr, *prec = nullptr;
+    uint32_t *nbr[2] = {nullptr, nullptr};  // TIER-3 neighbour ranks (A, S_hat), built on first use
     double *u[NU] = {}, *p[NP] = {};
     Geo geo{};
 };
@@ -440,6 +441,15 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         G.d0 = op == 0 ? S.u[U_D0] : S.p[P_SD0];
         G.d1 = op == 0 ? S.u[U_D1] : S.p[P_SD1];
         G.q = op == 0 ? S.u[U_CQ] : S.p[P_SQ];
+        if ((op == 0 ? c->plan_A : c->plan_S).tier == 3) {  // TIER 3 rank table, built on first use
+            uint32_t *&nb = S.nbr[op];
+            if (!nb) {
+                nb = c->alloc<uint32_t>((size_t)2 * c->dim * std::max<int64_t>(1, S.m_own[op]));
+                launch_build_nbr(c->dim, op, G, c->n, c->nw, nb, c->stream);
+                CK(cudaGetLastError());
+            }
+            G.nbr = nb;
+        }
         // k_cg1 buffers (the same slots, paired)
         G.zb[0] = G.z;
         G.zb[1] = G.r;
@@ -706,8 +716,12 @@ void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
         if (force == 1) return (int)CG_ONE_SUM;
         return m <= (int64_t)4 * nsm * CG_THREADS ? (int)CG_ONE_SUM : (int)CG_TWO_SUM;
     };
-    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max));
-    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max));
+    // TIER 3 (neighbour ranks precomputed in HBM) instead of bitmask lookups
+    // when the ranks do not fit the smem DOF cache: VOXSCHUR_NBR=1
+    const char *en = getenv("VOXSCHUR_NBR");
+    const bool nbr = en && atoi(en) == 1 && R == 1;
+    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max), nbr);
+    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max), nbr);
     // plane-sweep TMA tiles (k_cg1t): VOXSCHUR_TILED=1 turns them on
     const char *et = getenv("VOXSCHUR_TILED");
     if (et && atoi(et) == 1 && dim == 3 && R == 1 && !(C->nw & 1)) {

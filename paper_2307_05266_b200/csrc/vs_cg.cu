@@ -311,18 +311,18 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
 // Parity: values and iteration counts agree with the reference's
 // two-reduction form to rounding (tests/test_gpu_scale.py: counts within
 // 2 %, solutions within 1e-8); elementwise order is no longer bitwise.
-template <int DIM, int OP, int TIER>
-__global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
+template <int DIM, int OP, int TIER, int NT>
+__global__ void __launch_bounds__(NT, 1) k_cg1(const CgParams P) {
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
     constexpr int KS = PROJ ? 6 : 3;  // per-iteration sums
     extern __shared__ __align__(16) uint8_t dyn_smem[];
     __shared__ double s_tab[40];
-    __shared__ double s_warp[CG_THREADS / 32][5];
+    __shared__ double s_warp[NT / 32][5];
     __shared__ double s_tot[8];
     __shared__ CgGroup G;
-    // dynamic smem: [grid-sum staging KS x CG_THREADS doubles | DOF cache]
-    double(*s_val)[CG_THREADS] = reinterpret_cast<double(*)[CG_THREADS]>(dyn_smem);
+    // dynamic smem: [grid-sum staging KS x NT doubles | DOF cache]
+    double(*s_val)[NT] = reinterpret_cast<double(*)[NT]>(dyn_smem);
     if (threadIdx.x == 0) G = P.groups[P.group_base + blockIdx.x / P.bpg];
     if (threadIdx.x < 16) {
         s_tab[threadIdx.x] = P.diag_code[threadIdx.x];
@@ -331,13 +331,13 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
     }
     unsigned ep = __ldcg(P.bar_base);
     const uint32_t kc = P.cache_slots;
-    DofCache<DIM, OP, TIER> cache(dyn_smem + cg1_stage_bytes(OP), kc);
+    DofCache<DIM, OP, TIER, NT> cache(dyn_smem + cg1_stage_bytes(OP, NT), kc);
     __syncthreads();
     const Tabs T{s_tab, s_tab + 16, s_tab + 32, P.invS};
     const double2 *sdg = P.sdiag2;
     const uint32_t m = G.m_own;
-    const uint32_t tid = (blockIdx.x % P.bpg) * CG_THREADS + threadIdx.x;
-    const uint32_t stride = P.bpg * CG_THREADS;
+    const uint32_t tid = (blockIdx.x % P.bpg) * NT + threadIdx.x;
+    const uint32_t stride = P.bpg * NT;
     double *x = G.x, *dv = G.d0;
     __builtin_assume(__isGlobal(x));
     __builtin_assume(__isGlobal(dv));
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
     if (PROJ) {
         double v[1] = {0.0};
         for (uint32_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], G.rhs[i]);
-        grid_sum<1, false>(v, 0, P, ep, s_val, s_tot);
+        grid_sum<1, false, NT>(v, 0, P, ep, s_val, s_tot);
         mu_rhs = v[0] / P.m_global;
     }
     double mu, gamma, rp0, ru0;
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
             v[3] = __dadd_rn(v[3], zi);
             v[4] = __dadd_rn(v[4], ri);
         }
-        grid_sum_shfl<5, true>(v, 1, P, ep, s_warp, s_tot);
+        grid_sum_shfl<5, true, NT>(v, 1, P, ep, s_warp, s_tot);
         mu = PROJ ? v[3] / P.m_global : 0.0;
         gamma = PROJ ? __dsub_rn(v[0], __dmul_rn(mu, v[4])) : v[0];
         rp0 = sqrt(PROJ ? __dsub_rn(v[1], __dmul_rn(mu, v[3])) : v[1]);
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
         for (uint32_t i = tid; i < m; i += stride, ++k) {
             uint64_t rc;
             uint32_t nr[NS];
-            fetch_dof<DIM, OP, TIER>(P, G, cache, k, kc, i, rc, nr);
+            fetch_dof<DIM, OP, TIER, NT>(P, G, cache, k, kc, i, rc, nr);
             const double zi = zr[i];
             double vn[NS];
 #pragma unroll
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
             v[0] = __dadd_rn(v[0], __dmul_rn(zi, w));
             v[1] = __dadd_rn(v[1], w);
         }
-        grid_sum<2, true>(v, 2, P, ep, s_val, s_tot);
+        grid_sum<2, true, NT>(v, 2, P, ep, s_val, s_tot);
         delta = PROJ ? __dsub_rn(v[0], __dmul_rn(mu, v[1])) : v[0];
     }
     const double ref = rp0;
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
                 for (uint32_t i = tid; i < m; i += stride, ++k) {
                     uint64_t rc;
                     uint32_t nr[NS];
-                    fetch_dof<DIM, OP, TIER>(P, G, cache, k, kc, i, rc, nr);
+                    fetch_dof<DIM, OP, TIER, NT>(P, G, cache, k, kc, i, rc, nr);
                     const double zc = zr[i], uc = u[i], xc = x[i];
                     const double sc = first ? 0.0 : so[i], dc = first ? 0.0 : dv[i];
                     double vn[NS];
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
             // consecutive grid sums must use different partial sets: a block that
             // is one pass ahead writes the next sum while a slow block may still
             // read this one (same set -> diverging scalars -> barrier deadlock)
-            grid_sum<KS, true>(v, 3 - (int)(it & 1), P, ep, s_val, s_tot);
+            grid_sum<KS, true, NT>(v, 3 - (int)(it & 1), P, ep, s_val, s_tot);
             if (P.phase_ns && threadIdx.x == 0) {
                 const uint64_t t2 = gtimer();
                 ph[0] += t1 - t0;
@@ -552,41 +552,73 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_cg1(const CgParams P) {
 }
 
 template <int DIM, int OP>
-static const void *pcg_fn_t(int tier, int alg) {
-    if (alg == CG_ONE_SUM) return tier == 2 ? (const void *)k_cg1<DIM, OP, 2> : (const void *)k_cg1<DIM, OP, 1>;
-    return tier == 2 ? (const void *)k_pcg<DIM, OP, 2> : (const void *)k_pcg<DIM, OP, 1>;
+__global__ void k_build_nbr(const CgGroup G, int n, int nw, uint32_t *out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= G.m_own) return;
+    const uint64_t rc = G.rec[i];
+    uint32_t nr[2 * DIM];
+    neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), nw, n, G.nx, rc, i, nr);
+#pragma unroll
+    for (int s = 0; s < 2 * DIM; ++s) out[(size_t)s * G.m_own + i] = nr[s];
 }
-static const void *pcg_fn(int dim, int op, int tier, int alg) {
-    if (dim == 3) return op == 0 ? pcg_fn_t<3, 0>(tier, alg) : pcg_fn_t<3, 1>(tier, alg);
-    return op == 0 ? pcg_fn_t<2, 0>(tier, alg) : pcg_fn_t<2, 1>(tier, alg);
+void launch_build_nbr(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *out, cudaStream_t s) {
+    if (!G.m_own) return;
+    const unsigned nb = (G.m_own + 255) / 256;
+    if (dim == 3)
+        op == 0 ? k_build_nbr<3, 0><<<nb, 256, 0, s>>>(G, n, nw, out) : k_build_nbr<3, 1><<<nb, 256, 0, s>>>(G, n, nw, out);
+    else
+        op == 0 ? k_build_nbr<2, 0><<<nb, 256, 0, s>>>(G, n, nw, out) : k_build_nbr<2, 1><<<nb, 256, 0, s>>>(G, n, nw, out);
+}
+
+template <int DIM, int OP, int NT>
+static const void *cg1_fn_t(int tier) {
+    return tier == 3 ? (const void *)k_cg1<DIM, OP, 3, NT>
+                     : (tier == 2 ? (const void *)k_cg1<DIM, OP, 2, NT> : (const void *)k_cg1<DIM, OP, 1, NT>);
+}
+template <int DIM, int OP>
+static const void *pcg_fn_t(int tier, int alg, int nt) {
+    if (alg == CG_ONE_SUM) return nt == 512 ? cg1_fn_t<DIM, OP, 512>(tier) : cg1_fn_t<DIM, OP, CG_THREADS>(tier);
+    return tier == 3 ? (const void *)k_pcg<DIM, OP, 3>
+                     : (tier == 2 ? (const void *)k_pcg<DIM, OP, 2> : (const void *)k_pcg<DIM, OP, 1>);
+}
+static const void *pcg_fn(int dim, int op, int tier, int alg, int nt) {
+    if (dim == 3) return op == 0 ? pcg_fn_t<3, 0>(tier, alg, nt) : pcg_fn_t<3, 1>(tier, alg, nt);
+    return op == 0 ? pcg_fn_t<2, 0>(tier, alg, nt) : pcg_fn_t<2, 1>(tier, alg, nt);
 }
 
 // Plan one launch: blocks per group (all groups co-resident on one device),
 // cache tier and slots, smem.  m = the largest owned DOF count of a group.
-CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg) {
+CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, bool nbr_tier) {
     CgPlan pl{};
     pl.alg = alg;
+    // k_cg1 on the projected S_hat runs 512-thread blocks (B200, C1: 7.2 -> 6.1
+    // us/it: half the block-stage work in its 6-component grid sum); the A
+    // solve and k_pcg keep 1024 (k_pcg at 512: C2 S_hat 57 -> 83 us/it)
+    int nt = (alg == CG_ONE_SUM && op == 1) ? 512 : CG_THREADS;
+    if (const char *e = getenv("VOXSCHUR_CG1_THREADS"))
+        if (alg == CG_ONE_SUM && (atoi(e) == 512 || atoi(e) == CG_THREADS)) nt = atoi(e);
+    pl.threads = nt;
     int nsm = 0, maxopt = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     const int ns = 2 * dim;
-    for (int tier = 2; tier >= 1; --tier) {
-        const void *fn = pcg_fn(dim, op, tier, alg);
+    for (int tier : {2, nbr_tier ? 3 : 1}) {
+        const void *fn = pcg_fn(dim, op, tier, alg, nt);
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, fn);  // static smem (grid_sum staging, tables)
-        const size_t stage = alg == CG_ONE_SUM ? cg1_stage_bytes(op) : 0;  // dynamic grid-sum staging
+        const size_t stage = alg == CG_ONE_SUM ? cg1_stage_bytes(op, nt) : 0;  // dynamic grid-sum staging
         size_t total = std::min<size_t>(CG_SMEM_BUDGET + stage, (size_t)maxopt - fa.sharedSizeBytes);
         if (const char *e = getenv("VOXSCHUR_SMEM_KB")) total = std::min<size_t>(total, (size_t)atoi(e) * 1024 + stage);
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)total);
         const size_t budget = total - stage;  // DOF cache
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CG_THREADS, total);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, total);
         if (per_sm < 1) per_sm = 1;
         int grid = (int)std::max<int64_t>(
-            1, std::min<int64_t>((int64_t)per_sm * nsm / groups, (m + CG_THREADS - 1) / CG_THREADS));
-        const int64_t stride = (int64_t)grid * CG_THREADS;
+            1, std::min<int64_t>((int64_t)per_sm * nsm / groups, (m + nt - 1) / nt));
+        const int64_t stride = (int64_t)grid * nt;
         const int64_t slots = (m + stride - 1) / stride;
-        const size_t per_slot = (size_t)CG_THREADS * (tier == 2 ? 8 + 4 * ns : 8);
+        const size_t per_slot = (size_t)nt * (tier == 2 ? 8 + 4 * ns : 8);
         if (tier == 2 && (size_t)slots * per_slot > budget) continue;
         pl.tier = tier;
         pl.grid = grid;
@@ -602,7 +634,7 @@ cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &
     P.cache_slots = pl.slots;
     P.bpg = pl.grid;
     void *args[] = {&P};
-    return cudaLaunchCooperativeKernel(pcg_fn(dim, op, pl.tier, pl.alg), dim3(pl.grid * groups), dim3(CG_THREADS), args,
+    return cudaLaunchCooperativeKernel(pcg_fn(dim, op, pl.tier, pl.alg, pl.threads), dim3(pl.grid * groups), dim3(pl.threads), args,
                                        pl.smem, s);
 }
 

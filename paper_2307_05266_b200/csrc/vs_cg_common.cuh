@@ -332,33 +332,50 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
 // memory, the DOF's record (TIER >= 1) and its 2*DIM neighbour ranks
 // (TIER 2) for the first `kc` slots.  Cached DOFs skip the record read
 // (8 B/DOF/pass of DRAM) and, at TIER 2, the whole bitmask rank lookup.
-template <int DIM, int OP, int TIER>
+template <int DIM, int OP, int TIER, int NT = CG_THREADS>
 struct DofCache {
     static constexpr int NS = 2 * DIM;
     uint64_t *rec;
     uint32_t *rank;
     __device__ DofCache(uint8_t *base, uint32_t kc) {
         rec = reinterpret_cast<uint64_t *>(base);
-        rank = reinterpret_cast<uint32_t *>(base + (size_t)kc * CG_THREADS * 8);
+        rank = reinterpret_cast<uint32_t *>(base + (size_t)kc * NT * 8);
     }
     __device__ __forceinline__ void put(uint32_t k, uint64_t rc, const uint32_t (&nr)[NS]) {
-        rec[k * CG_THREADS + threadIdx.x] = rc;
+        rec[k * NT + threadIdx.x] = rc;
         if (TIER == 2) {
 #pragma unroll
-            for (int s = 0; s < NS; ++s) rank[(k * NS + s) * CG_THREADS + threadIdx.x] = nr[s];
+            for (int s = 0; s < NS; ++s) rank[(k * NS + s) * NT + threadIdx.x] = nr[s];
         }
     }
 };
 
-template <int DIM, int OP, int TIER>
-__device__ __forceinline__ void fetch_dof(const CgParams &P, const CgGroup &G, const DofCache<DIM, OP, TIER> &C,
+// TIER 3: records as TIER 1, neighbour ranks precomputed in global memory
+// (G.nbr, [2*DIM][m_own] uint32, streamed coalesced): the rank lookup is no
+// longer a dependent bitmask load between the record and the gathers.
+template <int DIM, int OP, int TIER, int NT = CG_THREADS>
+__device__ __forceinline__ void fetch_dof(const CgParams &P, const CgGroup &G, const DofCache<DIM, OP, TIER, NT> &C,
                                           uint32_t k, uint32_t kc, uint32_t i, uint64_t &rc,
                                           uint32_t (&nr)[2 * DIM]) {
+    if (TIER == 3) {
+        const uint32_t *nb = G.nbr;
+        __builtin_assume(__isGlobal(nb));
+#pragma unroll
+        for (int s = 0; s < 2 * DIM; ++s) nr[s] = __ldcs(nb + (size_t)s * G.m_own + i);
+        if (k < kc) {
+            rc = C.rec[k * NT + threadIdx.x];
+        } else {
+            const uint64_t *rec = G.rec;
+            __builtin_assume(__isGlobal(rec));
+            rc = rec[i];
+        }
+        return;
+    }
     if (k < kc) {
-        rc = C.rec[k * CG_THREADS + threadIdx.x];
+        rc = C.rec[k * NT + threadIdx.x];
         if (TIER == 2) {
 #pragma unroll
-            for (int s = 0; s < 2 * DIM; ++s) nr[s] = C.rank[(k * 2 * DIM + s) * CG_THREADS + threadIdx.x];
+            for (int s = 0; s < 2 * DIM; ++s) nr[s] = C.rank[(k * 2 * DIM + s) * NT + threadIdx.x];
             return;
         }
     } else {
@@ -370,7 +387,7 @@ __device__ __forceinline__ void fetch_dof(const CgParams &P, const CgGroup &G, c
 }
 
 // k_cg1 grid-sum staging in dynamic smem (KS rows of CG_THREADS doubles)
-__host__ __device__ constexpr size_t cg1_stage_bytes(int op) { return (size_t)(op == 1 ? 6 : 3) * CG_THREADS * 8; }
+__host__ __device__ constexpr size_t cg1_stage_bytes(int op, int nt = CG_THREADS) { return (size_t)(op == 1 ? 6 : 3) * nt * 8; }
 
 template <int OP>
 __device__ __forceinline__ void inv_diag(uint64_t rc, const Tabs &T, const double2 *__restrict__ sdg, double &inv,
