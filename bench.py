@@ -4,12 +4,16 @@
 Workload (N=1): BASELINE configs[1] -- 64^3 periodic sphere packing
 (radii U[4,8], porosity 0.4, x-percolating component), f=(1,0,0), solved
 once with Uzawa and once with SIMPLE at eps_S=1e-8, eps_A=eps_Shat=1e-12
-(SURVEY Appendix B).  One "step" = those two full Schur solves to tolerance.
+(SURVEY Appendix B).  One "step" = those two full Schur solves to tolerance,
+run concurrently on one GPU, each on its own system and share of the SMs
+(solve_schur_concurrent; shares in proportion to each solve's stand-alone
+time, measured in warm-up 1; --sequential runs them one after another).
 
 * value     -- masked-stencil Gcell/s = n^3 * (I_A + I_S) / t_device, I_A
                counting every inner A-iteration (incl. the u_f solve),
                I_S every inner S_hat-iteration; t_device = CUDA-event time
-               of the solves with the geometry resident in HBM.
+               span of the step's solves (first start to last end) with
+               the geometry resident in HBM.
 * e2e       -- same metric through the public API with host buffers:
                assemble(host mask) (H2D + device geometry build) and
                solve_schur returning p, u (D2H) inside the timed region.
@@ -208,7 +212,10 @@ def run_ours(a):
     grid = configs.make_geometry(a.config, a.seed)
     ncell = grid.fluid.size
     cfgs = [vx.SchurConfig(prec=p, max_iter=spec.max_iter, **TOL) for p in spec.precs]
-    sys_ = vx.assemble(grid, 0, check_connectivity=spec.check_connectivity, device=dev)
+    # one system (context: work vectors + stream) per preconditioner, so the
+    # step's independent solves can run concurrently on SM shares
+    systems = [vx.assemble(grid, 0, check_connectivity=spec.check_connectivity, device=dev) for _ in cfgs]
+    sys_ = systems[0]
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{dev}")  # 256 MB > L2
 
     def barrier():
@@ -216,13 +223,20 @@ def run_ours(a):
         if dist is not None:
             dist.barrier()
 
-    def one_step(s):
+    def one_step(weights):
         agg = dict(ms=0.0, IA=0, IS=0, dofA=0, dofS=0, msA=0.0, msS=0.0, launches=0,
                    lA=0, lS=0, reps=[], kA="", kS="")
-        for cfg in cfgs:
-            rep = vx.solve_schur(s, cfg, return_fields=False)
+        if weights is None:  # sequential, each solve on the whole device
+            reps = []
+            for s, cfg in zip(systems, cfgs):
+                s.limit_sms(0)
+                reps.append(vx.solve_schur(s, cfg, return_fields=False))
+            agg["ms"] = sum(r.device_ms for r in reps)
+        else:
+            reps = vx.solve_schur_concurrent(list(zip(systems, cfgs)), weights=weights, return_fields=False)
+            agg["ms"] = vx.schur.concurrent_span_ms(systems)
+        for s, cfg, rep in zip(systems, cfgs, reps):
             st = vx.last_kernel_stats(s)
-            agg["ms"] += rep.device_ms
             rtot = rep.inner_iter_totals
             agg["IA"] += st["velocity_cg"]["iterations"]
             agg["IS"] += st["simple_cg"]["iterations"]
@@ -236,20 +250,25 @@ def run_ours(a):
             agg["kA"] = st["velocity_cg"]["kernel"] or agg["kA"]
             if st["simple_cg"]["launches"]:
                 agg["kS"] = st["simple_cg"]["kernel"]
-            agg["reps"].append(dict(prec=cfg.prec, iters_outer=rep.iters_outer,
+            agg["reps"].append(dict(prec=cfg.prec, iters_outer=rep.iters_outer, sms=s.sms,
                                     inner=rtot, k=rep.k_value, converged=rep.converged,
                                     device_ms=rep.device_ms))
         return agg
 
-    for _ in range(a.warmup):
-        one_step(sys_)
+    # warm-up 1 runs the solves one after another on the whole device; its
+    # device times set the SM shares of the concurrent steps (a share in
+    # proportion to each solve's stand-alone time balances their spans)
+    seq = one_step(None)
+    weights = [r["device_ms"] for r in seq["reps"]] if len(cfgs) > 1 and not a.sequential else None
+    for _ in range(a.warmup - 1):
+        one_step(weights)
     barrier()
     steps = []
     with ClockSampler(dev) as clk:
         for _ in range(a.steps):
             flush.zero_()
             torch.cuda.synchronize(dev)
-            steps.append(one_step(sys_))
+            steps.append(one_step(weights))
         barrier()
     tot = {k: sum(st[k] for st in steps) for k in
            ("ms", "IA", "IS", "dofA", "dofS", "msA", "msS", "launches", "lA", "lS")}
@@ -274,21 +293,24 @@ def run_ours(a):
         flush.zero_()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        s2 = vx.assemble(grid, 0, check_connectivity=spec.check_connectivity, device=dev)
-        for cfg in cfgs:
-            rep = vx.solve_schur(s2, cfg, return_fields=True)
-            st = vx.last_kernel_stats(s2)
+        sy2 = [vx.assemble(grid, 0, check_connectivity=spec.check_connectivity, device=dev) for _ in cfgs]
+        if weights is None:
+            reps = [vx.solve_schur(s, cfg, return_fields=True) for s, cfg in zip(sy2, cfgs)]
+        else:
+            reps = vx.solve_schur_concurrent(list(zip(sy2, cfgs)), weights=weights, return_fields=True)
+        for s, rep in zip(sy2, reps):
+            st = vx.last_kernel_stats(s)
             e2e_cells += ncell * (st["velocity_cg"]["iterations"] + st["simple_cg"]["iterations"])
             d2h += rep.pressure.nbytes + rep.velocity.nbytes + 5 * 8 * (rep.iters_outer + 1)
         e2e_t += time.perf_counter() - t0
-        h2d += grid.fluid.size  # uint8 mask
-        del s2
+        h2d += grid.fluid.size * len(cfgs)  # uint8 mask, one upload per system
+        del sy2
     nsteps_e2e = max(1, a.steps)
     e2e = {"value": e2e_cells / e2e_t / 1e9, "unit": "Gcell/s",
            "h2d_bytes_per_step": h2d // nsteps_e2e, "d2h_bytes_per_step": d2h // nsteps_e2e,
            "ms_per_step": 1e3 * e2e_t / nsteps_e2e,
-           "includes": "assemble (host connectivity check + H2D mask + device geometry build) "
-                       "+ solves + D2H p,u,histories"}
+           "includes": "assemble of one system per solve (host connectivity check + H2D mask + device "
+                    "geometry build) + solves (concurrent as in the timed steps) + D2H p,u,histories"}
 
     peak, peak_kind = measured_peak()
     # dominant kernel: the fused persistent PCG with the larger share
@@ -356,11 +378,16 @@ def run_ours(a):
             "config": {"workload": spec.name, "seed": a.seed, "n": grid.n,
                        "porosity": float(grid.fluid.mean()), "m_u": sys_.m_u, "m_p": sys_.m_p,
                        "precs": list(spec.precs), "tolerances": TOL,
-                       "step": "one full solve_schur to tolerance per preconditioner",
+                       "step": "one full solve_schur to tolerance per preconditioner"
+                               + (", run concurrently on SM shares (solve_schur_concurrent); step time = "
+                                  "device span from the first start to the last end (CUDA events)"
+                                  if weights else ", one after another"),
+                       "sm_shares": {r["prec"]: r["sms"] for r in steps[-1]["reps"]},
                        "l2": "256 MB buffer written between timed steps (L2 flushed)",
                        "parallelism": f"replicas{world}" if world > 1 else "single"},
             "hbm_gbs_algorithmic": hbm_alg,
-            "time_to_tol_ms": {r["prec"]: r["device_ms"] for r in last},
+            # each solve alone on the whole device (warm-up 1, CUDA events)
+            "time_to_tol_ms": {r["prec"]: r["device_ms"] for r in seq["reps"]},
             "solves": last,
             "inner_iterations_per_step": {"A": tot["IA"] // a.steps, "S_hat": tot["IS"] // a.steps},
             "roofline": roofline, "roofline_hbm_regime": hbm, "cpu_baseline": cpu, "e2e": e2e,
@@ -383,6 +410,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-hbm", action="store_true", help="skip the C2 HBM-regime kernel measurement")
+    ap.add_argument("--sequential", action="store_true",
+                    help="run the step's solves one after another on the whole device")
     a = ap.parse_args()
     if a.warmup < 3:
         print("warning: the timing rules require --warmup >= 3", file=sys.stderr)

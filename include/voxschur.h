@@ -99,6 +99,19 @@ int vs_ctx_create2(const uint8_t *fluid, int dim, int n, int flow_dir,
                    double inv_h, double inv_h2, int slabs, vs_ctx **out);
 int vs_slab_count(vs_ctx *ctx);
 
+/* Plan the fused inner solves of a single-slab context on `sms` SMs
+ * (0 = the whole device), so that independent solves on separate contexts
+ * (e.g. the two preconditioners, or a sweep's geometries) run concurrently
+ * on disjoint SM shares, each on its context's own stream.  No reference
+ * counterpart: the reference runs independent solves in a process pool
+ * (cli.py:205-212). */
+int vs_ctx_limit_sms(vs_ctx *ctx, int sms);
+int vs_ctx_sms(vs_ctx *ctx);
+/* Device time (CUDA events) from the start of the last vs_solve_schur on
+ * `first` to the end of the last one on `last` (same device): the span of
+ * concurrent solves is the max over pairs. */
+int vs_solve_span_ms(vs_ctx *first, vs_ctx *last, double *ms);
+
 /* Multi-GPU, one process per GPU: context for rank `rank` of `nranks`
  * (slab decomposition as vs_ctx_create2 with slabs = nranks, but this process
  * holds only its own slab, in one device arena).  Exchange the 64-byte

@@ -18,6 +18,7 @@ from .schur import (
     profile_config,
     schur_rhs,
     solve_schur,
+    solve_schur_concurrent,
 )
 
 __version__ = "0.1.0"
@@ -28,5 +29,6 @@ __all__ = [
     "DofMap", "StaggeredSystem", "assemble", "axis_index", "connect_ranks",
     "TOLERANCE_PROFILES", "SchurConfig", "SolveReport", "apply_schur", "apply_simple_inverse",
     "last_kernel_stats", "permeability", "profile_config", "schur_rhs", "solve_schur",
+    "solve_schur_concurrent",
     "__version__",
 ]

@@ -81,6 +81,9 @@ def _load():
         "vs_ctx_create2": (C.c_int, [u8, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                      C.c_double, C.c_double, C.c_int, C.POINTER(P)]),
         "vs_slab_count": (C.c_int, [P]),
+        "vs_ctx_limit_sms": (C.c_int, [P, C.c_int]),
+        "vs_ctx_sms": (C.c_int, [P]),
+        "vs_solve_span_ms": (C.c_int, [P, P, C.POINTER(C.c_double)]),
         "vs_slab_plan": (C.c_int, [u8, C.c_int, C.c_int, C.c_int, P]),
         "vs_ctx_create_rank": (C.c_int, [u8, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(P)]),
@@ -110,7 +113,7 @@ def _load():
 
 lib = _load()
 EXPORTED = (
-    "vs_last_error", "vs_version", "vs_components", "vs_stamp_balls", "vs_ctx_create", "vs_ctx_create2", "vs_slab_count", "vs_slab_plan", "vs_ctx_create_rank", "vs_ipc_handle", "vs_ipc_attach",
+    "vs_last_error", "vs_version", "vs_components", "vs_stamp_balls", "vs_ctx_create", "vs_ctx_create2", "vs_slab_count", "vs_ctx_limit_sms", "vs_ctx_sms", "vs_solve_span_ms", "vs_slab_plan", "vs_ctx_create_rank", "vs_ipc_handle", "vs_ipc_attach",
     "vs_ctx_destroy",
     "vs_counts", "vs_export_geometry", "vs_apply_laplacian", "vs_apply_divergence",
     "vs_apply_gradient", "vs_divergence_weighted_diagonal", "vs_apply_simple",

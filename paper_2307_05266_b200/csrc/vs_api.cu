@@ -56,6 +56,18 @@ struct Status {
 }  // namespace
 
 namespace {
+// The device's default stream-ordered pool keeps freed memory instead of
+// returning it to the driver at each synchronisation, so a context built
+// after another one was destroyed allocates without driver calls.
+void keep_pool(int device) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+}
+}  // namespace
+
+namespace {
 
 // ----------------------------------------------------------------- slabs
 // Vector slots of a slab.  Velocity slots have m_all[0] entries, pressure
@@ -93,7 +105,7 @@ struct vs_ctx {
     double inv_h = 0, inv_h2 = 0, diag_scale = 0;
     double diag_code[16] = {0}, inv_code[16] = {0}, invA_enc[8] = {0};
     bool sdiag_ok = true;
-    std::vector<void *> allocs;
+    std::vector<void *> allocs, ipc_allocs;
     // global geometry (reference numbering)
     uint32_t *fbits = nullptr;
     uint2 *vmeta[3] = {nullptr, nullptr, nullptr};
@@ -119,6 +131,8 @@ struct vs_ctx {
     double *h_scal = nullptr;  // pinned
     CgOut *h_cg = nullptr;     // pinned
     CgPlan plan_A{}, plan_S{};
+    int64_t mu_max = 0, mp_max = 0;  // largest slab's owned DOFs (the plans' sizes)
+    int sms = 0;                     // SMs the fused solves are planned on
     TilePlan tile_A{}, tile_S{};  // k_cg1t plans (one slab, 3D); used when use_tile[op]
     bool use_tile[2] = {false, false};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
@@ -134,18 +148,31 @@ struct vs_ctx {
         g.pmeta = pmeta;
         return g;
     }
+    // Device memory comes from the device's stream-ordered pool (released
+    // back to the pool, not the driver, on destroy): building and destroying
+    // contexts costs no device-wide synchronisation and reuses the memory of
+    // earlier contexts.  The slab arena of a multi-process context is an
+    // ordinary allocation (it is exported with cudaIpcGetMemHandle).
     template <class T>
     T *alloc(size_t count) {
         void *p = nullptr;
-        CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+        CK(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), stream));
         allocs.push_back(p);
+        return (T *)p;
+    }
+    template <class T>
+    T *alloc_ipc(size_t count) {
+        void *p = nullptr;
+        CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+        ipc_allocs.push_back(p);
         return (T *)p;
     }
     ~vs_ctx() {
         if (device >= 0) cudaSetDevice(device);
         if (tile_A.mem) cudaFree(tile_A.mem);
         if (tile_S.mem) cudaFree(tile_S.mem);
-        for (void *p : allocs) cudaFree(p);
+        for (void *p : allocs) cudaFreeAsync(p, stream);
+        for (void *p : ipc_allocs) cudaFree(p);
         if (h_scal) cudaFreeHost(h_scal);
         if (h_cg) cudaFreeHost(h_cg);
         if (h_groups) cudaFreeHost(h_groups);
@@ -669,6 +696,8 @@ void bind_arena(Slab &S, char *base, const ArenaLayout &L) {
     for (int k = 0; k < NP; ++k) S.p[k] = (double *)(base + L.p[k]);
 }
 
+void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms);
+
 // Build the decomposition from the global geometry: R slabs in total, of
 // which this process holds [s0, s1) (all of them, or `rank`'s one).
 void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
@@ -700,28 +729,9 @@ void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
         mu_max = std::max(mu_max, S.m_own[0]);
         mp_max = std::max(mp_max, S.m_own[1]);
     }
-    // one-reduction CG on a single slab; the slab decomposition keeps the
-    // two-reduction loop (its halo exchange is built for it).
-    // VOXSCHUR_CG=2 forces the two-reduction loop everywhere.
-    // It pays where the grid sums dominate (a few DOFs per thread; B200 C1
-    // 64^3: A 12.4 -> 9.7, S_hat 9.6 -> 8.5 us/it); on large solves its
-    // 18 gathers per DOF cost more than the saved sum (C2 S_hat 57.6 -> 63.3).
-    // VOXSCHUR_CG=1 / =2 forces the one- / two-reduction loop.
-    const char *ea = getenv("VOXSCHUR_CG");
-    const int force = ea ? atoi(ea) : 0;
-    int nsm = 0;
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, C->device));
-    auto pick = [&](int64_t m) {
-        if (R > 1 || force == 2) return (int)CG_TWO_SUM;
-        if (force == 1) return (int)CG_ONE_SUM;
-        return m <= (int64_t)4 * nsm * CG_THREADS ? (int)CG_ONE_SUM : (int)CG_TWO_SUM;
-    };
-    // TIER 3 (neighbour ranks precomputed in HBM) instead of bitmask lookups
-    // when the ranks do not fit the smem DOF cache: VOXSCHUR_NBR=1
-    const char *en = getenv("VOXSCHUR_NBR");
-    const bool nbr = en && atoi(en) == 1 && R == 1;
-    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max), nbr);
-    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max), nbr);
+    C->mu_max = mu_max;
+    C->mp_max = mp_max;
+    plan_solvers(C, mu_max, mp_max, 0);
     // plane-sweep TMA tiles (k_cg1t): VOXSCHUR_TILED=1 turns them on
     const char *et = getenv("VOXSCHUR_TILED");
     if (et && atoi(et) == 1 && dim == 3 && R == 1 && !(C->nw & 1)) {
@@ -770,7 +780,7 @@ void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
         for (int a = 0; a < 3; ++a) S.geo.vmeta[a] = S.meta[a];
         S.geo.pmeta = S.meta[FP];
         const ArenaLayout L = arena_layout(S, C->tb_max, R);
-        char *base = C->alloc<char>(L.bytes);
+        char *base = nranks > 1 ? C->alloc_ipc<char>(L.bytes) : C->alloc<char>(L.bytes);
         bind_arena(S, base, L);
         if (s == C->s0) {
             C->arena = base;
@@ -805,6 +815,35 @@ void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
     CK(cudaMallocHost(&C->h_cglog, C->cglog_cap * sizeof(CgOut)));
     C->ost = C->alloc<OuterState>(1);
     CK(cudaMallocHost(&C->h_ost, sizeof(OuterState)));
+}
+
+// Fused-PCG plans of both inner operators on `sms` SMs (0: the whole device).
+// One-reduction CG (k_cg1) on a single slab where the grid sums dominate (a
+// few DOFs per thread; B200 C1 64^3: A 12.4 -> 9.7, S_hat 9.6 -> 8.5 us/it);
+// on large solves its 18 gathers per DOF cost more than the saved sum (C2
+// S_hat 57.6 -> 63.3), and the slab decomposition keeps the two-reduction
+// loop (its halo exchange is built for it).  VOXSCHUR_CG=1 / =2 forces the
+// one- / two-reduction loop.  TIER 3 (neighbour ranks precomputed in HBM)
+// instead of bitmask lookups when the ranks do not fit the smem DOF cache:
+// VOXSCHUR_NBR=1.
+void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
+    const int R = C->R, dim = C->dim;
+    const int nloc = C->s1 - C->s0;
+    const char *ea = getenv("VOXSCHUR_CG");
+    const int force = ea ? atoi(ea) : 0;
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, C->device));
+    if (sms > 0 && sms < nsm) nsm = sms;
+    auto pick = [&](int64_t m) {
+        if (R > 1 || force == 2) return (int)CG_TWO_SUM;
+        if (force == 1) return (int)CG_ONE_SUM;
+        return m <= (int64_t)4 * nsm * CG_THREADS ? (int)CG_ONE_SUM : (int)CG_TWO_SUM;
+    };
+    const char *en = getenv("VOXSCHUR_NBR");
+    const bool nbr = en && atoi(en) == 1 && R == 1;
+    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max), nbr, nsm);
+    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max), nbr, nsm);
+    C->sms = nsm;
 }
 
 }  // namespace
@@ -961,6 +1000,7 @@ static int create_common(const uint8_t *fluid, int dim, int n, int flow_dir, int
     vs_ctx *C = c.get();
     int rc = guarded(C, [&] {
         CK(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking));
+        keep_pool(device);
         for (cudaEvent_t *e : {&C->ev0, &C->ev1, &C->evs0, &C->evs1}) CK(cudaEventCreate(e));
         CK(cudaMallocHost(&C->h_scal, 8 * sizeof(double)));
         CK(cudaMallocHost(&C->h_cg, sizeof(CgOut)));
@@ -1430,5 +1470,23 @@ int vs_kernel_stats(vs_ctx *c, vs_kstat *a, vs_kstat *s, int64_t *launches) {
 }
 
 int vs_slab_count(vs_ctx *c) { return c->R; }
+
+int vs_ctx_limit_sms(vs_ctx *c, int sms) {
+    if (sms < 0) return fail(VS_EVALUE, "sms must be >= 0, got %d", sms);
+    if (c->R > 1 || c->use_tile[0] || c->use_tile[1])
+        return fail(VS_EVALUE, "SM limit applies to single-slab contexts without tiled solves");
+    // grids only shrink, so the buffers sized for tb_max still fit
+    return guarded(c, [&] { plan_solvers(c, c->mu_max, c->mp_max, sms); });
+}
+
+int vs_ctx_sms(vs_ctx *c) { return c->sms; }
+
+int vs_solve_span_ms(vs_ctx *first, vs_ctx *last, double *ms) {
+    return guarded(first, [&] {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, first->ev0, last->ev1));
+        *ms = t;
+    });
+}
 
 }  // extern "C"

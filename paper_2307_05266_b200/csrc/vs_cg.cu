@@ -588,7 +588,7 @@ static const void *pcg_fn(int dim, int op, int tier, int alg, int nt) {
 
 // Plan one launch: blocks per group (all groups co-resident on one device),
 // cache tier and slots, smem.  m = the largest owned DOF count of a group.
-CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, bool nbr_tier) {
+CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, bool nbr_tier, int sms) {
     CgPlan pl{};
     pl.alg = alg;
     // k_cg1 on the projected S_hat runs 512-thread blocks (B200, C1: 7.2 -> 6.1
@@ -601,6 +601,7 @@ CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, boo
     int nsm = 0, maxopt = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (sms > 0 && sms < nsm) nsm = sms;  // a share of the device (concurrent solves)
     const int ns = 2 * dim;
     for (int tier : {2, nbr_tier ? 3 : 1}) {
         const void *fn = pcg_fn(dim, op, tier, alg, nt);

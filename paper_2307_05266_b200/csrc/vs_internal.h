@@ -122,7 +122,8 @@ struct CgPlan {
     uint32_t slots;
     size_t smem;
 };
-CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, bool nbr_tier = false);
+CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, bool nbr_tier = false,
+                int sms = 0);
 // fill the TIER-3 neighbour-rank table of one group's owned DOFs
 void launch_build_nbr(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *out, cudaStream_t s);
 cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);

@@ -168,6 +168,18 @@ class StaggeredSystem:
         return self._apply(_lib.lib.vs_divergence_weighted_diagonal, face_weights,
                            self._m_u, self._m_p, "face weight")
 
+    def limit_sms(self, sms: int) -> None:
+        """Plan this system's fused inner solves on ``sms`` SMs (0 = all).
+
+        For independent solves on separate systems that run concurrently
+        (``solve_schur_concurrent``); no reference counterpart."""
+        _lib.check(_lib.lib.vs_ctx_limit_sms(self._ctx, int(sms)))
+
+    @property
+    def sms(self) -> int:
+        """SMs the fused inner solves are planned on."""
+        return int(_lib.lib.vs_ctx_sms(self._ctx))
+
     def apply_simple(self, p) -> np.ndarray:
         """B diag(A)^-1 B^T p in one kernel (schur.py:234-240)."""
         return self._apply(_lib.lib.vs_apply_simple, p, self._m_p, self._m_p, "pressure")
