@@ -6,8 +6,8 @@ Workload (N=1): BASELINE configs[1] -- 64^3 periodic sphere packing
 once with Uzawa and once with SIMPLE at eps_S=1e-8, eps_A=eps_Shat=1e-12
 (SURVEY Appendix B).  One "step" = those two full Schur solves to tolerance,
 run concurrently on one GPU, each on its own system and share of the SMs
-(solve_schur_concurrent; shares in proportion to each solve's stand-alone
-time, measured in warm-up 1; --sequential runs them one after another).
+(solve_schur_concurrent; the split is tuned in untimed warm-up steps, see
+"sm_split_tuning_ms"; --sequential runs them one after another).
 
 * value     -- masked-stencil Gcell/s = n^3 * (I_A + I_S) / t_device, I_A
                counting every inner A-iteration (incl. the u_f solve),
@@ -223,17 +223,17 @@ def run_ours(a):
         if dist is not None:
             dist.barrier()
 
-    def one_step(weights):
+    def one_step(shares):
         agg = dict(ms=0.0, IA=0, IS=0, dofA=0, dofS=0, msA=0.0, msS=0.0, launches=0,
-                   lA=0, lS=0, reps=[], kA="", kS="")
-        if weights is None:  # sequential, each solve on the whole device
+                   lA=0, lS=0, reps=[], per_kernel={})
+        if shares is None:  # sequential, each solve on the whole device
             reps = []
             for s, cfg in zip(systems, cfgs):
                 s.limit_sms(0)
                 reps.append(vx.solve_schur(s, cfg, return_fields=False))
             agg["ms"] = sum(r.device_ms for r in reps)
         else:
-            reps = vx.solve_schur_concurrent(list(zip(systems, cfgs)), weights=weights, return_fields=False)
+            reps = vx.solve_schur_concurrent(list(zip(systems, cfgs)), sms=shares, return_fields=False)
             agg["ms"] = vx.schur.concurrent_span_ms(systems)
         for s, cfg, rep in zip(systems, cfgs, reps):
             st = vx.last_kernel_stats(s)
@@ -247,28 +247,56 @@ def run_ours(a):
             agg["lA"] += st["velocity_cg"]["launches"]
             agg["lS"] += st["simple_cg"]["launches"]
             agg["launches"] += st["kernel_launches"]
-            agg["kA"] = st["velocity_cg"]["kernel"] or agg["kA"]
-            if st["simple_cg"]["launches"]:
-                agg["kS"] = st["simple_cg"]["kernel"]
+            # per fused-CG kernel and operator (a split can run the same
+            # operator through different kernels in the two systems)
+            for key, op in (("velocity_cg", "A"), ("simple_cg", "S_hat,proj")):
+                if st[key]["launches"]:
+                    kk = agg["per_kernel"].setdefault(f"{st[key]['kernel']}<{op}>", [0, 0.0, 0, 0])
+                    kk[0] += st[key]["dof_iters"]
+                    kk[1] += st[key]["ms"]
+                    kk[2] += st[key]["launches"]
+                    kk[3] = s.sms
             agg["reps"].append(dict(prec=cfg.prec, iters_outer=rep.iters_outer, sms=s.sms,
                                     inner=rtot, k=rep.k_value, converged=rep.converged,
                                     device_ms=rep.device_ms))
         return agg
 
-    # warm-up 1 runs the solves one after another on the whole device; its
-    # device times set the SM shares of the concurrent steps (a share in
-    # proportion to each solve's stand-alone time balances their spans)
+    # warm-up 1 runs the solves one after another on the whole device.  With
+    # two solves, untimed tuning steps then pick the SM split: a coarse scan
+    # around the split in proportion to the stand-alone times, then a fine
+    # one around the best (per-iteration time steps with the DOFs per thread
+    # of the fused CG, so the best split is not the proportional one).
     seq = one_step(None)
-    weights = [r["device_ms"] for r in seq["reps"]] if len(cfgs) > 1 and not a.sequential else None
+    shares, tuning = None, []
+    if len(cfgs) == 2 and not a.sequential:
+        total = systems[0].sms
+        t = [r["device_ms"] for r in seq["reps"]]
+        prop = int(round(total * t[1] / (t[0] + t[1])))
+        tried = {}
+
+        def trial(k1):
+            k1 = min(max(k1, 1), total - 1)
+            if k1 not in tried:
+                tried[k1] = one_step([total - k1, k1])["ms"]
+            return tried[k1]
+
+        for k1 in range(prop - 24, prop + 25, 4):
+            trial(k1)
+        best = min(tried, key=tried.get)
+        for k1 in range(best - 3, best + 4):
+            trial(k1)
+        best = min(tried, key=tried.get)
+        shares = [total - best, best]
+        tuning = sorted(([total - k, k, round(v, 1)] for k, v in tried.items()), key=lambda r: r[1])
     for _ in range(a.warmup - 1):
-        one_step(weights)
+        one_step(shares)
     barrier()
     steps = []
     with ClockSampler(dev) as clk:
         for _ in range(a.steps):
             flush.zero_()
             torch.cuda.synchronize(dev)
-            steps.append(one_step(weights))
+            steps.append(one_step(shares))
         barrier()
     tot = {k: sum(st[k] for st in steps) for k in
            ("ms", "IA", "IS", "dofA", "dofS", "msA", "msS", "launches", "lA", "lS")}
@@ -294,15 +322,16 @@ def run_ours(a):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         sy2 = [vx.assemble(grid, 0, check_connectivity=spec.check_connectivity, device=dev) for _ in cfgs]
-        if weights is None:
+        if shares is None:
             reps = [vx.solve_schur(s, cfg, return_fields=True) for s, cfg in zip(sy2, cfgs)]
         else:
-            reps = vx.solve_schur_concurrent(list(zip(sy2, cfgs)), weights=weights, return_fields=True)
+            reps = vx.solve_schur_concurrent(list(zip(sy2, cfgs)), sms=shares, return_fields=True)
         for s, rep in zip(sy2, reps):
             st = vx.last_kernel_stats(s)
             e2e_cells += ncell * (st["velocity_cg"]["iterations"] + st["simple_cg"]["iterations"])
             d2h += rep.pressure.nbytes + rep.velocity.nbytes + 5 * 8 * (rep.iters_outer + 1)
         e2e_t += time.perf_counter() - t0
+        print(f"e2e step {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr)
         h2d += grid.fluid.size * len(cfgs)  # uint8 mask, one upload per system
         del sy2
     nsteps_e2e = max(1, a.steps)
@@ -313,24 +342,39 @@ def run_ours(a):
                     "geometry build) + solves (concurrent as in the timed steps) + D2H p,u,histories"}
 
     peak, peak_kind = measured_peak()
-    # dominant kernel: the fused persistent PCG with the larger share
-    domS = tot["msS"] >= tot["msA"]
-    dof_k, ms_k, l_k = (tot["dofS"], tot["msS"], tot["lS"]) if domS else (tot["dofA"], tot["msA"], tot["lA"])
+
+    # dominant kernel: the fused persistent PCG (kernel, operator) with the
+    # largest summed launch time over the timed steps
+    perk = {}
+    for st in steps:
+        for k, (d, ms, l, nsm) in st["per_kernel"].items():
+            acc = perk.setdefault(k, [0, 0.0, 0, 0])
+            acc[0] += d
+            acc[1] += ms
+            acc[2] += l
+            acc[3] = nsm
+    kname = max(perk, key=lambda k: perk[k][1])
+    dof_k, ms_k, l_k, sms_k = perk[kname]
     achieved = BYTES_PER_DOF_ITER * dof_k / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)
-        traffic = tj.get(a.config, {}).get("k_pcg_S" if domS else "k_pcg_A")
+        traffic = tj.get(a.config, {}).get(kname)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": (f"{steps[-1]['kS']}<S_hat,proj> (fused persistent PCG)" if domS
-                           else f"{steps[-1]['kA']}<A> (fused persistent PCG)"),
+                "kernel": f"{kname} (fused persistent PCG)",
                 "launches": l_k, "avg_launch_ms": ms_k / max(1, l_k),
                 "bytes_per_launch": BYTES_PER_DOF_ITER * dof_k / max(1, l_k),
                 "peak_kind": peak_kind, "frac_vs_8TBs": achieved / 8000.0,
-                "share_of_step": (ms_k / tot["ms"]) if tot["ms"] else None}
+                # kernel time / step span; above 1 when the step's solves overlap
+                "share_of_step": (ms_k / tot["ms"]) if tot["ms"] else None,
+                # the kernel runs on its solve's SM share, not the whole device
+                "sms": sms_k,
+                "kernels": {k: {"launches": v[2], "ms": round(v[1], 3), "sms": v[3],
+                                "achieved_gbs": BYTES_PER_DOF_ITER * v[0] / (v[1] / 1e3) / 1e9 if v[1] else 0.0}
+                            for k, v in perk.items()}}
 
     # HBM regime: the same fused kernels on C2 (256^3, working set > L2), one
     # inner A-solve and one inner S_hat-solve (SURVEY 8d per-iteration roofline)
@@ -381,8 +425,9 @@ def run_ours(a):
                        "step": "one full solve_schur to tolerance per preconditioner"
                                + (", run concurrently on SM shares (solve_schur_concurrent); step time = "
                                   "device span from the first start to the last end (CUDA events)"
-                                  if weights else ", one after another"),
+                                  if shares else ", one after another"),
                        "sm_shares": {r["prec"]: r["sms"] for r in steps[-1]["reps"]},
+                       "sm_split_tuning_ms": tuning,
                        "l2": "256 MB buffer written between timed steps (L2 flushed)",
                        "parallelism": f"replicas{world}" if world > 1 else "single"},
             "hbm_gbs_algorithmic": hbm_alg,
