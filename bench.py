@@ -395,13 +395,20 @@ def run_ours(a):
             torch.cuda.synchronize(dev)
             vx.apply_simple_inverse(s2, pz, 1e-12)
             stS = vx.last_kernel_stats(s2)["simple_cg"]
-        def rl(st):
+        tj = {}
+        if os.path.exists(os.path.join(ROOT, "profiles", "traffic.json")):
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                tj = json.load(f).get("C2", {})
+
+        def rl(st, op):
             ach = BYTES_PER_DOF_ITER * st["dof_iters"] / (st["ms"] / 1e3) / 1e9
             return {"kernel": st["kernel"], "iterations": st["iterations"],
-                    "us_per_iteration": 1e3 * st["ms"] / st["iterations"], "achieved": ach, "frac": ach / peak}
+                    "us_per_iteration": 1e3 * st["ms"] / st["iterations"], "achieved": ach, "frac": ach / peak,
+                    "algorithmic_bytes": BYTES_PER_DOF_ITER * st["dof_iters"],
+                    "traffic": tj.get(f"{st['kernel']}<{op}>")}
         hbm = {"workload": "C2 256^3 spheres phi0.15 (m_u %d, m_p %d): one inner A-solve and one inner "
                            "S_hat-solve to 1e-12" % (s2.m_u, s2.m_p),
-               "unit": "GB/s", "peak": peak, "k_pcg_A": rl(stA), "k_pcg_S": rl(stS)}
+               "unit": "GB/s", "peak": peak, "k_pcg_A": rl(stA, "A"), "k_pcg_S": rl(stS, "S_hat,proj")}
         del s2
 
     line = None

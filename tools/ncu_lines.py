@@ -31,5 +31,6 @@ for f in sorted({k[0] for k in agg}):
     ti = sum(v[1] for _, v in rows) or 1
     ts = sum(v[2] for _, v in rows) or 1
     print(f"== {f[:70]}  warp-inst {ti:.3e}  samples {ts}")
-    for (_, p, ln), (src, ni, ns) in sorted(rows, key=lambda kv: -kv[1][1])[:top]:
+    order = 2 if "--by-stall" in sys.argv else 1
+    for (_, p, ln), (src, ni, ns) in sorted(rows, key=lambda kv: -kv[1][order])[:top]:
         print(f"  {p}:{ln:<5d} inst {100 * ni / ti:5.1f}%  stall {100 * ns / ts:5.1f}%  {src[:80]}")
