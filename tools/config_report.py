@@ -40,7 +40,11 @@ def slit_k(n: int, w: int, wall: int = 4) -> float:
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    argv = sys.argv[1:]
+    if "--cap-c4" in argv:  # drop the option and its value
+        i = argv.index("--cap-c4")
+        argv = argv[:i] + argv[i + 2:]
+    args = [a for a in argv if not a.startswith("--")]
     cap = 3
     if "--cap-c4" in sys.argv:
         cap = int(sys.argv[sys.argv.index("--cap-c4") + 1])
@@ -58,7 +62,7 @@ def main():
             max_iter = spec.max_iter
             if key == "C2" and prec == "uzawa":
                 max_iter = 5000  # BASELINE configs[2]: Uzawa capped at 5000 outer iterations
-            capped = key.startswith("C4")
+            capped = key.startswith("C4") and cap < spec.max_iter
             if capped:
                 max_iter = cap
             cfg = vx.SchurConfig(prec=prec, max_iter=max_iter, **TOL)
