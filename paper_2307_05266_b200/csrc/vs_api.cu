@@ -502,7 +502,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     }
     CgGroup *dg = c->d_groups + ring * nloc;
     CK(cudaMemcpyAsync(dg, hg, nloc * sizeof(CgGroup), cudaMemcpyHostToDevice, c->stream));
-    CgParams P;
+    CgParams P{};
     memset(&P, 0, sizeof P);
     P.groups = dg;
     P.group_base = 0;  // groups[] holds this process's slabs only
@@ -513,6 +513,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.bar = c->bar;
     P.bar_base = c->bar_base;
     P.npart = c->npart;
+    P.xgpu = c->mp() ? 1 : 0;
     P.part_self = c->mp() ? c->rank : 0;
     for (int r = 0; r < c->npart; ++r) P.part_peer[r] = c->part_peer[r];
     P.phase_ns = c->phase_ns;

@@ -159,14 +159,28 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
 // (the reds form one release sequence); it is 0.13 us cheaper than a
 // fence.acq_rel (B200, 148 x 1024 threads: 1.17 vs 1.30 us per barrier;
 // the unfenced floor is 0.84 us -- tools/gridsync_variants.cu).
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, unsigned total_blocks) {
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, unsigned total_blocks,
+                                             bool xgpu = false) {
     __syncthreads();
     target += total_blocks;
     if (threadIdx.x == 0) {
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-        while ((int)(ld_relaxed(bar) - target) < 0) {
+        if (xgpu) {
+            // ranks on different GPUs (peer memory over NVLink): system scope,
+            // so the release orders this GPU's peer stores (ghost planes,
+            // partials) before the arrival, and the acquire makes the other
+            // GPUs' stores visible here
+            asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+            unsigned v;
+            do {
+                asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            } while ((int)(v - target) < 0);
+            asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.sys.global.u32 t, [%0];\n\t}" ::"l"(bar) : "memory");
+        } else {
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+            while ((int)(ld_relaxed(bar) - target) < 0) {
+            }
+            asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.gpu.global.u32 t, [%0];\n\t}" ::"l"(bar) : "memory");
         }
-        asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.gpu.global.u32 t, [%0];\n\t}" ::"l"(bar) : "memory");
     }
     __syncthreads();
 }
@@ -224,7 +238,7 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
             for (int k = 0; k < K; ++k) dst[k] = t[k];
         }
     }
-    grid_barrier(P.bar, target, TB);  // starts with __syncthreads (s_warp reuse is safe)
+    grid_barrier(P.bar, target, TB, P.xgpu);  // starts with __syncthreads (s_warp reuse is safe)
     // own buffer: one per rank (per group when ranks are emulated as groups)
     const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +
                          (size_t)set * 8 * TB;
@@ -301,7 +315,7 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
             *dst = t[0];
         }
     }
-    grid_barrier(P.bar, target, TB);  // starts with __syncthreads (s_val reuse is safe)
+    grid_barrier(P.bar, target, TB, P.xgpu);  // starts with __syncthreads (s_val reuse is safe)
     if (warp < K) {
         // own buffer: one per rank (per group when ranks are emulated as groups)
         const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +

@@ -54,6 +54,7 @@ struct CgParams {
     int total_blocks;       // blocks of all ranks in this solve
     int block_base;         // global index of this launch's block 0
     int npart;              // ranks whose partial buffers receive this launch's sums
+    int xgpu;               // ranks are processes on different GPUs: system-scope barrier
     int part_self;          // index in part_peer of the first local group's own buffer
     double *part_peer[VS_MAX_SLABS];
     CgOut *out;

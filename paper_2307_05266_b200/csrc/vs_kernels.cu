@@ -417,15 +417,16 @@ __global__ void k_outer(int op, OuterState *st, const double *scal, int R, doubl
 }
 
 // cross-rank barrier for the outer loop: one arrival per rank on the
-// counter the fused CG uses (its base carried in *bar_base)
+// counter the fused CG uses (its base carried in *bar_base).  The ranks are
+// processes on different GPUs, so release/acquire are at system scope.
 __global__ void k_xbar(unsigned *bar, unsigned *bar_base, int nranks) {
     const unsigned target = *bar_base + (unsigned)nranks;
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     unsigned v;
     do {
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
     } while ((int)(v - target) < 0);
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
     *bar_base = target;
 }
 void launch_xbar(unsigned *bar, unsigned *bar_base, int nranks, cudaStream_t s) {
