@@ -280,11 +280,16 @@ def run_ours(a):
                 tried[k1] = one_step([total - k1, k1])["ms"]
             return tried[k1]
 
-        for k1 in range(prop - 24, prop + 25, 4):
-            trial(k1)
-        best = min(tried, key=tried.get)
-        for k1 in range(best - 3, best + 4):
-            trial(k1)
+        # the scan costs ~19 steps: only for steps that take seconds at most
+        # (C1); longer workloads use the proportional split
+        if max(t) < 2000.0:
+            for k1 in range(prop - 24, prop + 25, 4):
+                trial(k1)
+            best = min(tried, key=tried.get)
+            for k1 in range(best - 3, best + 4):
+                trial(k1)
+        else:
+            trial(prop)
         best = min(tried, key=tried.get)
         shares = [total - best, best]
         tuning = sorted(([total - k, k, round(v, 1)] for k, v in tried.items()), key=lambda r: r[1])
