@@ -74,7 +74,9 @@ int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels,
  * solidify, in order, the periodic balls (or, with prism_axis >= 0,
  * cylinders along that axis) of the given centres/radii (cell-index
  * coordinates, minimum-image distance <= r) until the fluid count drops
- * to target_fluid or the list ends.  *used = balls consumed. */
+ * to target_fluid or the list ends.  *used = balls consumed.  *n_fluid is
+ * in/out: on entry the current fluid count of the mask, or < 0 to count
+ * it; on return the count after stamping. */
 int vs_stamp_balls(uint8_t *fluid, int dim, int n, const double *centers,
                    const double *radii, int64_t count, int64_t target_fluid,
                    int prism_axis, int64_t *used, int64_t *n_fluid);

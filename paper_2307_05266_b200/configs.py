@@ -32,8 +32,8 @@ __all__ = ["ConfigSpec", "CONFIGS", "make_geometry", "balls", "slits", "x_percol
 BATCH = 4096
 
 
-def _stamp(fluid: np.ndarray, centers, radii, target: int, prism_axis: int):
-    used, nf = C.c_int64(), C.c_int64()
+def _stamp(fluid: np.ndarray, centers, radii, target: int, prism_axis: int, n_fluid: int = -1):
+    used, nf = C.c_int64(), C.c_int64(n_fluid)
     flat = fluid.reshape(-1)
     _lib.check(_lib.lib.vs_stamp_balls(
         _lib.ptr(flat), fluid.ndim, fluid.shape[0], _lib.ptr(np.ascontiguousarray(centers)),
@@ -53,10 +53,11 @@ def balls(n: int, dim: int, rmin: float, rmax: float, *, porosity: float | None 
         _stamp(fluid, c, r, -1, prism_axis)
         return fluid.astype(bool)
     target = int(np.floor(porosity * fluid.size))
+    nf = fluid.size
     while True:
         c = rng.uniform(0, n, size=(BATCH, dim))
         r = rng.uniform(rmin, rmax, size=BATCH)
-        used, nf = _stamp(fluid, c, r, target, prism_axis)
+        used, nf = _stamp(fluid, c, r, target, prism_axis, nf)
         if nf <= target:
             return fluid.astype(bool)
 

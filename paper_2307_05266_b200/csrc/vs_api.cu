@@ -871,10 +871,21 @@ int vs_stamp_balls(uint8_t *fluid, int dim, int n, const double *centers, const 
                    int64_t target_fluid, int prism_axis, int64_t *used, int64_t *n_fluid) {
     if ((dim != 2 && dim != 3) || n < 2) return fail(VS_EVALUE, "bad grid for vs_stamp_balls");
     const int64_t N = dim == 3 ? (int64_t)n * n * n : (int64_t)n * n;
-    int64_t nf = 0;
-    for (int64_t i = 0; i < N; ++i) nf += fluid[i] ? 1 : 0;
+    // *n_fluid >= 0 on entry: the caller's running fluid count (a batched
+    // caller passes back the previous call's result; recounting n^3 cells
+    // per batch dominated 1024^3 generation)
+    int64_t nf = *n_fluid;
+    if (nf < 0) {
+        nf = 0;
+        for (int64_t i = 0; i < N; ++i) nf += fluid[i] ? 1 : 0;
+    }
     int64_t k = 0;
     const int64_t st[3] = {dim == 3 ? (int64_t)n * n : (int64_t)n, dim == 3 ? (int64_t)n : 1, 1};
+    constexpr int WMAX = 4096;  // window positions per axis of the hoisted path
+    std::vector<int64_t> woff_v(3 * WMAX);
+    std::vector<double> wd2_v(3 * WMAX);
+    int64_t *woff[3] = {woff_v.data(), woff_v.data() + WMAX, woff_v.data() + 2 * WMAX};
+    double *wd2[3] = {wd2_v.data(), wd2_v.data() + WMAX, wd2_v.data() + 2 * WMAX};
     for (; k < count && nf > target_fluid; ++k) {
         const double r = radii[k], r2 = r * r;
         const double *c = centers + k * dim;
@@ -886,22 +897,54 @@ int vs_stamp_balls(uint8_t *fluid, int dim, int n, const double *centers, const 
             if (hi[a] - lo[a] + 1 > n) { lo[a] = 0; hi[a] = n - 1; }
         }
         if (dim == 2) { lo[2] = hi[2] = 0; }
-        for (int i = lo[0]; i <= hi[0]; ++i)
-            for (int j = lo[1]; j <= hi[1]; ++j)
-                for (int l = lo[2]; l <= hi[2]; ++l) {
-                    const int idx[3] = {i, j, l};
-                    double d2 = 0.0;
-                    int64_t off = 0;
-                    for (int a = 0; a < dim; ++a) {
-                        const int w = ((idx[a] % n) + n) % n;  // periodic wrap of the window
-                        off += w * st[dim == 3 ? a : (a == 0 ? 0 : 2)];
-                        if (a == prism_axis) continue;
-                        double dd = std::fabs((double)w - c[a]);
-                        dd = std::min(dd, (double)n - dd);  // minimum image
-                        d2 += dd * dd;
-                    }
-                    if (d2 <= r2 && fluid[off]) { fluid[off] = 0; --nf; }
+        // per axis: wrapped index offset and squared minimum-image distance
+        // of every window position (same operations as per cell, hoisted)
+        int len[3] = {1, 1, 1};
+        bool small = true;
+        for (int a = 0; a < 3; ++a) {
+            len[a] = hi[a] - lo[a] + 1;
+            if (len[a] > WMAX) small = false;
+        }
+        if (small) {
+            for (int a = 0; a < dim; ++a)
+                for (int t = 0; t < len[a]; ++t) {
+                    const int w = (((lo[a] + t) % n) + n) % n;
+                    woff[a][t] = (int64_t)w * st[dim == 3 ? a : (a == 0 ? 0 : 2)];
+                    double dd = std::fabs((double)w - c[a]);
+                    dd = std::min(dd, (double)n - dd);
+                    wd2[a][t] = a == prism_axis ? 0.0 : dd * dd;
                 }
+            if (dim == 2) { woff[2][0] = 0; wd2[2][0] = 0.0; }
+            for (int ti = 0; ti < len[0]; ++ti)
+                for (int tj = 0; tj < len[1]; ++tj) {
+                    // d2 accumulates axis by axis from 0.0, as below (a prism
+                    // axis contributes nothing: adding 0.0 is exact)
+                    const double d01 = (0.0 + wd2[0][ti]) + wd2[1][tj];
+                    const int64_t o01 = woff[0][ti] + woff[1][tj];
+                    for (int tl = 0; tl < len[2]; ++tl) {
+                        const double d2 = dim == 3 ? d01 + wd2[2][tl] : d01;
+                        const int64_t off = o01 + woff[2][tl];
+                        if (d2 <= r2 && fluid[off]) { fluid[off] = 0; --nf; }
+                    }
+                }
+        } else {
+            for (int i = lo[0]; i <= hi[0]; ++i)
+                for (int j = lo[1]; j <= hi[1]; ++j)
+                    for (int l = lo[2]; l <= hi[2]; ++l) {
+                        const int idx[3] = {i, j, l};
+                        double d2 = 0.0;
+                        int64_t off = 0;
+                        for (int a = 0; a < dim; ++a) {
+                            const int w = ((idx[a] % n) + n) % n;  // periodic wrap of the window
+                            off += w * st[dim == 3 ? a : (a == 0 ? 0 : 2)];
+                            if (a == prism_axis) continue;
+                            double dd = std::fabs((double)w - c[a]);
+                            dd = std::min(dd, (double)n - dd);  // minimum image
+                            d2 += dd * dd;
+                        }
+                        if (d2 <= r2 && fluid[off]) { fluid[off] = 0; --nf; }
+                    }
+        }
         if (nf <= target_fluid) { ++k; break; }
     }
     *used = k;

@@ -140,3 +140,52 @@ def test_pcg_errors_and_lanczos():
     assert lo == pytest.approx(1.0, abs=1e-8) and hi == pytest.approx(4.0, abs=1e-8)
     with pytest.raises(ValueError, match="nonpositive"):
         vx.jacobi_prec(np.array([1.0, 0.0]))
+
+
+# ---- seeded config generator (configs.py, native stamper) -----------------
+
+
+def _stamp_numpy(n, dim, centers, radii, target, prism_axis=-1):
+    """Plain restatement of the stamping rule: in order, every cell whose
+    minimum-image distance (squared, summed axis by axis from 0.0, the prism
+    axis skipped) to a ball centre is <= r^2 becomes solid, until the fluid
+    count drops to ``target``."""
+    fluid = np.ones((n,) * dim, dtype=bool)
+    idx = np.indices(fluid.shape)
+    nf = fluid.size
+    used = 0
+    for c, r in zip(centers, radii):
+        if nf <= target:
+            break
+        d2 = np.zeros(fluid.shape)
+        for a in range(dim):
+            if a == prism_axis:
+                continue
+            dd = np.abs(idx[a].astype(float) - c[a])
+            dd = np.minimum(dd, n - dd)
+            d2 = d2 + dd * dd
+        hit = (d2 <= r * r) & fluid
+        fluid[hit] = False
+        nf -= int(hit.sum())
+        used += 1
+    return fluid, used, nf
+
+
+@pytest.mark.parametrize("dim,n,prism", [(3, 24, -1), (3, 20, 0), (2, 40, -1)])
+def test_stamp_balls_matches_rule(dim, n, prism):
+    from paper_2307_05266_b200 import configs
+
+    rng = np.random.default_rng(3)
+    c = rng.uniform(0, n, size=(60, dim))
+    r = rng.uniform(1.5, 4.5, size=60)
+    target = int(0.5 * n**dim)
+    ref, used_ref, nf_ref = _stamp_numpy(n, dim, c, r, target, prism)
+    fl = np.ones((n,) * dim, dtype=np.uint8)
+    used, nf = configs._stamp(fl, c, r, target, prism)           # counts the mask itself
+    assert (used, nf) == (used_ref, nf_ref) and np.array_equal(fl.astype(bool), ref)
+    fl2 = np.ones((n,) * dim, dtype=np.uint8)
+    half = 30
+    u1, nf1 = configs._stamp(fl2, c[:half], r[:half], target, prism)  # batched, running count
+    if nf1 > target:
+        u2, nf1 = configs._stamp(fl2, c[half:], r[half:], target, prism, nf1)
+    assert nf1 == nf_ref and np.array_equal(fl2.astype(bool), ref)
