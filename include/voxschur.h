@@ -70,6 +70,12 @@ const char *vs_version(void);
 int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels,
                   int64_t *n_components);
 
+/* The same labelling on the GPU `device` (lock-free union-find, roots at
+ * the minimum cell index, dense ids by a scan of the roots): identical
+ * labels and count.  assemble uses it for grids of >= 2^22 cells. */
+int vs_components_device(const uint8_t *fluid, int dim, int n, int device, int32_t *labels,
+                         int64_t *n_components);
+
 /* Seeded synthetic geometry (BASELINE configs; not a reference function):
  * solidify, in order, the periodic balls (or, with prism_axis >= 0,
  * cylinders along that axis) of the given centres/radii (cell-index

@@ -110,8 +110,9 @@ for _w in (2, 4, 8, 16, 32):
                                      check_connectivity=False)
 
 
-def make_geometry(key: str, seed: int = 0, n: int | None = None) -> VoxelGrid:
-    """The fluid grid of config ``key`` (optionally at a different n, for tests)."""
+def make_geometry(key: str, seed: int = 0, n: int | None = None, device: int | None = None) -> VoxelGrid:
+    """The fluid grid of config ``key`` (optionally at a different n, for tests).
+    ``device``: run the connected-component labelling on that GPU."""
     spec = CONFIGS[key]
     n = spec.n if n is None else n
     if spec.kind == "slits":
@@ -122,7 +123,7 @@ def make_geometry(key: str, seed: int = 0, n: int | None = None) -> VoxelGrid:
     else:
         fluid = balls(n, spec.dim, spec.rmin, spec.rmax, porosity=spec.porosity,
                       count=spec.count, seed=seed)
-    grid, _ = enforce_connectivity(VoxelGrid(fluid))
+    grid, _ = enforce_connectivity(VoxelGrid(fluid), device)
     if not x_percolates(grid.fluid):
         raise ValueError(f"{key} seed {seed}: kept component does not reach every x-plane")
     return grid

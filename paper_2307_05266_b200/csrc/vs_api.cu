@@ -867,6 +867,36 @@ int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels, int64_t
     return VS_OK;
 }
 
+int vs_components_device(const uint8_t *fluid, int dim, int n, int device, int32_t *labels, int64_t *n_components) {
+    if ((dim != 2 && dim != 3) || n < 1) return fail(VS_EVALUE, "grid dimension must be 2 or 3, got %d", dim);
+    const int64_t N = dim == 3 ? (int64_t)n * n * n : (int64_t)n * n;
+    if (N >= ((int64_t)1 << 31)) return fail(VS_EVALUE, "grid of %lld cells exceeds the int32 labelling", (long long)N);
+    try {
+        CK(cudaSetDevice(device));
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        uint8_t *d_f = nullptr;
+        int *d_lab = nullptr;
+        void *work = nullptr;
+        const size_t wb = cc_work_bytes(N);
+        CK(cudaMallocAsync(&d_f, N, s));
+        CK(cudaMallocAsync(&work, wb, s));
+        if (labels) CK(cudaMallocAsync(&d_lab, N * sizeof(int), s));
+        CK(cudaMemcpyAsync(d_f, fluid, N, cudaMemcpyHostToDevice, s));
+        *n_components = cc_label_device(d_f, dim, n, d_lab, work, wb, s);
+        if (labels) CK(cudaMemcpyAsync(labels, d_lab, N * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaFreeAsync(d_f, s));
+        CK(cudaFreeAsync(work, s));
+        if (d_lab) CK(cudaFreeAsync(d_lab, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaStreamDestroy(s));
+        CK(cudaGetLastError());
+    } catch (const CudaFail &e) {
+        return fail(VS_ECUDA, "CUDA error %s in %s", cudaGetErrorString(e.e), e.what);
+    }
+    return VS_OK;
+}
+
 int vs_stamp_balls(uint8_t *fluid, int dim, int n, const double *centers, const double *radii, int64_t count,
                    int64_t target_fluid, int prism_axis, int64_t *used, int64_t *n_fluid) {
     if ((dim != 2 && dim != 3) || n < 2) return fail(VS_EVALUE, "bad grid for vs_stamp_balls");
@@ -1017,7 +1047,11 @@ static int create_common(const uint8_t *fluid, int dim, int n, int flow_dir, int
     for (int64_t i = 0; i < ncells; ++i) nfluid += fluid[i] ? 1 : 0;
     if (nfluid == 0) return fail(VS_EVALUE, "empty fluid domain");
     if (require_walls && nfluid == ncells) return fail(VS_EVALUE, "velocity operator singular: no no-slip boundary");
-    if (check_connectivity) {
+    // small grids: host union-find before any device work; large grids
+    // (>= CC_DEVICE_CELLS): the same labelling on the GPU after the mask
+    // upload (vs_cc.cu; 1024^3 on the host took seconds per pass)
+    const bool cc_on_device = check_connectivity && ncells >= CC_DEVICE_CELLS;
+    if (check_connectivity && !cc_on_device) {
         int64_t nc = 0;
         try {
             nc = label_components(fluid, dim, n, nullptr);
@@ -1052,6 +1086,21 @@ static int create_common(const uint8_t *fluid, int dim, int n, int flow_dir, int
         // ---- K1: mask -> bits -> face bits -> ranks -> records
         uint8_t *d_fluid = C->alloc<uint8_t>(ncells);
         CK(cudaMemcpyAsync(d_fluid, fluid, ncells, cudaMemcpyHostToDevice, C->stream));
+        if (cc_on_device) {  // operators.py:224-230
+            const size_t wb = cc_work_bytes(ncells);
+            void *work = nullptr;
+            CK(cudaMallocAsync(&work, wb, C->stream));
+            const int64_t nc = cc_label_device(d_fluid, dim, n, nullptr, work, wb, C->stream);
+            CK(cudaFreeAsync(work, C->stream));
+            CK(cudaGetLastError());
+            if (nc > 1) {
+                char buf[160];
+                snprintf(buf, sizeof buf,
+                         "fluid domain is disconnected (%lld components); run enforce_connectivity first",
+                         (long long)nc);
+                throw Status{VS_EVALUE, buf};
+            }
+        }
         C->fbits = C->alloc<uint32_t>(nw);
         Geo g = C->geo();
         launch_pack_fluid(d_fluid, g, nw, C->fbits, C->stream);

@@ -114,6 +114,11 @@ void launch_outer(int op, OuterState *st, const double *scal, int R, double arg,
 void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s);
 int launch_reduce(int kind, const double *a, const double *b, int64_t m, double *part, double *out,
                   cudaStream_t s);
+// connected components on the GPU (vs_cc.cu)
+constexpr int64_t CC_DEVICE_CELLS = (int64_t)1 << 22;  // assemble checks larger grids on the device
+size_t cc_work_bytes(int64_t N);
+int64_t cc_label_device(const uint8_t *d_fluid, int dim, int n, int *d_labels, void *work, size_t work_bytes,
+                        cudaStream_t s);
 constexpr size_t CG_SMEM_BUDGET = 200 * 1024;  // dynamic smem per block (1 block / SM)
 enum CgAlg { CG_TWO_SUM = 0, CG_ONE_SUM = 1 };  // k_pcg (reference order) | k_cg1 (one reduction)
 struct CgPlan {

@@ -47,22 +47,32 @@ class VoxelGrid:
         return self.fluid.shape[0]
 
 
-def connected_components(grid: VoxelGrid):
+def connected_components(grid: VoxelGrid, device: int | None = None):
     """Label fluid components under periodic face adjacency.
 
     Returns ``(labels, n_components)``; labels are -1 on solid and dense
     ids in first row-major appearance on fluid (geometry.py:183-190).
+    With ``device`` the labelling runs on that GPU (same labels).
     """
+    labels, n = _labels32(grid, device)
+    return labels.astype(np.int64), n
+
+
+def _labels32(grid: VoxelGrid, device: int | None):
     f = np.ascontiguousarray(grid.fluid, dtype=np.uint8)
     labels = np.empty(f.shape, dtype=np.int32)
     n = C.c_int64()
-    _lib.check(_lib.lib.vs_components(f.ravel(), grid.dim, grid.n, _lib.ptr(labels), C.byref(n)))
-    return labels.astype(np.int64), int(n.value)
+    if device is None:
+        _lib.check(_lib.lib.vs_components(f.ravel(), grid.dim, grid.n, _lib.ptr(labels), C.byref(n)))
+    else:
+        _lib.check(_lib.lib.vs_components_device(f.ravel(), grid.dim, grid.n, int(device), _lib.ptr(labels),
+                                                 C.byref(n)))
+    return labels, int(n.value)
 
 
-def enforce_connectivity(grid: VoxelGrid):
+def enforce_connectivity(grid: VoxelGrid, device: int | None = None):
     """Solidify everything outside the largest component (ties: lowest id)."""
-    labels, n = connected_components(grid)
+    labels, n = _labels32(grid, device)
     if n == 0:
         raise ValueError("empty fluid domain")
     if n == 1:
