@@ -34,6 +34,8 @@ extern "C" {
 #define VS_EVALUE 1
 #define VS_ERUNTIME 2
 #define VS_ECUDA 3
+#define VS_EOS 4      /* open/read/write failed; message = errno (the reference raises OSError) */
+#define VS_EDECODE 5  /* file is not UTF-8 (the reference raises UnicodeDecodeError) */
 
 typedef struct vs_ctx vs_ctx;
 
@@ -75,6 +77,16 @@ int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels,
  * labels and count.  assemble uses it for grids of >= 2^22 cells. */
 int vs_components_device(const uint8_t *fluid, int dim, int n, int device, int32_t *labels,
                          int64_t *n_components);
+
+/* voxgeo text IO (geometry.py:243-339), multithreaded host C++.
+ * vs_grid_header: dim and size from the three header lines only (to size
+ * the caller's buffer); vs_read_grid: the whole file with the reference's
+ * checks and messages, into fluid (C-order (x,y,z), 1 = fluid; cap bytes;
+ * fluid may be NULL to validate only); vs_write_grid: the reference's exact
+ * bytes. */
+int vs_grid_header(const char *path, int *dim, int64_t *n);
+int vs_read_grid(const char *path, uint8_t *fluid, int64_t cap, int *dim, int64_t *n);
+int vs_write_grid(const char *path, const uint8_t *fluid, int dim, int64_t n);
 
 /* Seeded synthetic geometry (BASELINE configs; not a reference function):
  * solidify, in order, the periodic balls (or, with prism_axis >= 0,

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VOXSCHUR_LIB", os.path.join(_HERE, "libvoxschur.so"))
 
-VS_OK, VS_EVALUE, VS_ERUNTIME, VS_ECUDA = 0, 1, 2, 3
+VS_OK, VS_EVALUE, VS_ERUNTIME, VS_ECUDA, VS_EOS, VS_EDECODE = 0, 1, 2, 3, 4, 5
 
 
 class VsReport(C.Structure):
@@ -104,6 +104,9 @@ def _load():
                                      P, P, P, P, P]),
         "vs_kernel_stats": (C.c_int, [P, C.POINTER(VsKstat), C.POINTER(VsKstat), i64p]),
         "vs_phase_timing": (C.c_int, [P, dp]),
+        "vs_grid_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), i64p]),
+        "vs_read_grid": (C.c_int, [C.c_char_p, P, C.c_int64, C.POINTER(C.c_int), i64p]),
+        "vs_write_grid": (C.c_int, [C.c_char_p, P, C.c_int, C.c_int64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)  # AttributeError here = the ABI is incomplete
@@ -119,7 +122,7 @@ EXPORTED = (
     "vs_counts", "vs_export_geometry", "vs_apply_laplacian", "vs_apply_divergence",
     "vs_apply_gradient", "vs_divergence_weighted_diagonal", "vs_apply_simple",
     "vs_solve_velocity", "vs_solve_simple", "vs_solve_schur", "vs_kernel_stats",
-    "vs_phase_timing",
+    "vs_phase_timing", "vs_grid_header", "vs_read_grid", "vs_write_grid",
 )
 
 

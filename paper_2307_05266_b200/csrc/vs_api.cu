@@ -55,6 +55,10 @@ struct Status {
 
 }  // namespace
 
+namespace vs {
+void set_last_error(const std::string &msg) { g_err = msg; }
+}  // namespace vs
+
 namespace {
 // The device's default stream-ordered pool keeps freed memory instead of
 // returning it to the driver at each synchronisation, so a context built
