@@ -67,6 +67,10 @@ const char *vs_last_error(void);
 /* Library build string (arch, version). */
 const char *vs_version(void);
 
+/* Visible CUDA devices (0 when there is no device or driver); the sweep
+ * driver binds one worker per device. */
+int vs_device_count(int *count);
+
 /* Periodic face-adjacency components of a mask (geometry.py:183-222).
  * labels (nullable) receives ids in first row-major appearance, -1 on solid. */
 int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels,

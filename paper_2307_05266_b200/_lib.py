@@ -104,6 +104,7 @@ def _load():
                                      P, P, P, P, P]),
         "vs_kernel_stats": (C.c_int, [P, C.POINTER(VsKstat), C.POINTER(VsKstat), i64p]),
         "vs_phase_timing": (C.c_int, [P, dp]),
+        "vs_device_count": (C.c_int, [C.POINTER(C.c_int)]),
         "vs_grid_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), i64p]),
         "vs_read_grid": (C.c_int, [C.c_char_p, P, C.c_int64, C.POINTER(C.c_int), i64p]),
         "vs_write_grid": (C.c_int, [C.c_char_p, P, C.c_int, C.c_int64]),
@@ -122,7 +123,7 @@ EXPORTED = (
     "vs_counts", "vs_export_geometry", "vs_apply_laplacian", "vs_apply_divergence",
     "vs_apply_gradient", "vs_divergence_weighted_diagonal", "vs_apply_simple",
     "vs_solve_velocity", "vs_solve_simple", "vs_solve_schur", "vs_kernel_stats",
-    "vs_phase_timing", "vs_grid_header", "vs_read_grid", "vs_write_grid",
+    "vs_phase_timing", "vs_device_count", "vs_grid_header", "vs_read_grid", "vs_write_grid",
 )
 
 

@@ -861,6 +861,15 @@ const char *vs_last_error(void) { return g_err.c_str(); }
 
 const char *vs_version(void) { return "voxschur 0.2 sm_100a (fp64, fused persistent PCG, x-slab groups)"; }
 
+int vs_device_count(int *count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) c = 0;
+    else if (e != cudaSuccess) return fail(VS_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+    *count = c;
+    return VS_OK;
+}
+
 int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels, int64_t *n_components) {
     if ((dim != 2 && dim != 3) || n < 1) return fail(VS_EVALUE, "grid dimension must be 2 or 3, got %d", dim);
     try {

@@ -152,9 +152,46 @@ def packing_cases():
     return out, rej
 
 
+def cli_cases():
+    """The reference CLI's sweep and solve outputs on the sizes its own
+    tests use (test_cli.py:17-25, :155-160); the ``time`` column and
+    ``wall_time`` are dropped."""
+    from voxstokes.cli import main as ref_main, read_csv_rows
+
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        g = os.path.join(d, "g.vox")
+        assert ref_main(["gen", "--N", "1", "--nc", "10", "--navg", "4", "--nmin", "2",
+                         "--seed", "7", "-o", g]) == 0
+        solves = {}
+        for name, extra in (("simple_paper2d", ["--prec", "simple", "--profile", "paper2d"]),
+                            ("uzawa_unprec", ["--prec", "uzawa", "--eps-s", "1e-3", "--norm",
+                                              "unprec", "--eps-a", "1e-13"])):
+            base = os.path.join(d, name)
+            assert ref_main(["solve", g, *extra, "-o", base]) == 0
+            with open(base + ".json") as fh:
+                rep = json.load(fh)
+            rep.pop("wall_time")
+            solves[name] = {"argv": extra, "report": rep}
+        out["solve"] = solves
+        sd = os.path.join(d, "sweep")
+        argv = ["sweep", "--N", "2", "--nc", "10", "--nmin", "2", "--navg", "4", "6", "--seed",
+                "3", "--prec", "both", "--profile", "paper2d", "--jobs", "1", "-o", sd]
+        assert ref_main(argv) == 0
+        sweep = {"argv": argv[:-2]}
+        for name in ("summary", "thresholds", "correlation"):
+            rows = read_csv_rows(os.path.join(sd, f"{name}.csv"))
+            for row in rows:
+                row.pop("time", None)
+            sweep[name] = rows
+        out["sweep"] = sweep
+    return out
+
+
 def main():
     packing, rejected = packing_cases()
-    doc = {"read": read_cases(), "packing": packing, "packing_rejected": rejected}
+    doc = {"read": read_cases(), "packing": packing, "packing_rejected": rejected,
+           "cli": cli_cases()}
     with open(os.path.join(HERE, "io_cases.json"), "w") as fh:
         json.dump(doc, fh, indent=1)
         fh.write("\n")
