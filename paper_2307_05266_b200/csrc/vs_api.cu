@@ -839,15 +839,23 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     int nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, C->device));
     if (sms > 0 && sms < nsm) nsm = sms;
-    auto pick = [&](int64_t m) {
-        if (R > 1 || force == 2) return (int)CG_TWO_SUM;
-        if (force == 1) return (int)CG_ONE_SUM;
-        return m <= (int64_t)4 * nsm * CG_THREADS ? (int)CG_ONE_SUM : (int)CG_TWO_SUM;
+    // Two-reduction loop: q by recurrence (k_pcg<QR>, 6 gathers per DOF
+    // instead of 12) for the A-solve at every size (B200: C2 132.5 -> 123.5,
+    // C4 512^3 1780 -> 1546 us/it) and for S_hat above kQrecS DOFs (C4 512^3
+    // 836 -> 804 us/it; at C2 it loses, 57.1 -> 60.0).  VOXSCHUR_CG=2 forces
+    // the reference-order q = A d everywhere, =3 the recurrence everywhere.
+    constexpr int64_t kQrecS = 8 << 20;
+    auto pick = [&](int64_t m, int op) {
+        if (force == 3) return (int)CG_TWO_SUM_QREC;
+        if (force == 2) return (int)CG_TWO_SUM;
+        if (R == 1 && (force == 1 || (force == 0 && m <= (int64_t)4 * nsm * CG_THREADS)))
+            return (int)CG_ONE_SUM;
+        return (op == 0 || m > kQrecS) ? (int)CG_TWO_SUM_QREC : (int)CG_TWO_SUM;
     };
     const char *en = getenv("VOXSCHUR_NBR");
     const bool nbr = en && atoi(en) == 1 && R == 1;
-    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max), nbr, nsm);
-    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max), nbr, nsm);
+    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max, 0), nbr, nsm);
+    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max, 1), nbr, nsm);
     C->sms = nsm;
 }
 

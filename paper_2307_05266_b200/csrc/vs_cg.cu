@@ -28,7 +28,13 @@
 namespace vs {
 
 
-template <int DIM, int OP, int TIER>
+// QR: q by recurrence, q = A(z - mu) + beta q_old (A applied to the projected
+// z, then the reference's d-recurrence carried over to q by linearity; the
+// same recurrence k_cg1 uses for s = M q).  P1 then gathers the neighbours'
+// z only (6 loads instead of 12 in 3D) and reads its own q_old; neighbour d
+// is never needed, so the ghost-plane d recompute goes too.  Rounding
+// differs from q = A d at the last bits (not bitwise the reference's order).
+template <int DIM, int OP, int TIER, bool QR = false>
 __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
@@ -146,6 +152,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                     }
                     double zc = z[i];
                     const double dc = first ? 0.0 : dold[i];
+                    const double qo = (QR && !first) ? q[i] : 0.0;
                     uint64_t rc;
                     uint32_t nr[NS];
                     fetch_dof<DIM, OP, TIER>(P, G, cache, k, kc, i, rc, nr);
@@ -154,7 +161,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                     for (int s = 0; s < NS; ++s) {  // unconditional loads (absent -> own index)
                         const uint32_t j = nr[s] != ABSENT ? nr[s] : i;
                         zn[s] = z[j];
-                        dn[s] = first ? 0.0 : dold[j];
+                        dn[s] = (first || QR) ? 0.0 : dold[j];
                     }
                     if (PROJ) zc = __dsub_rn(zc, mu);
                     const double di = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dc));
@@ -163,17 +170,25 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                     for (int s = 0; s < NS; ++s) {
                         double zj = zn[s];
                         if (PROJ) zj = __dsub_rn(zj, mu);
-                        const double dj = first ? zj : __dadd_rn(zj, __dmul_rn(beta, dn[s]));
+                        const double dj = (first || QR) ? zj : __dadd_rn(zj, __dmul_rn(beta, dn[s]));
                         // A needs 0.0 at absent slots (left fold); S_hat's absent faces
                         // carry weight 0.0 (op_value), so the clamped value is harmless
                         vn[s] = (OP == 0 && nr[s] == ABSENT) ? 0.0 : dj;
                     }
-                    const double qi = op_value<DIM, OP>(rc, di, vn, T, inv_h, inv_h2);
+                    double qi;
+                    if (QR) {
+                        const double wi = op_value<DIM, OP>(rc, zc, vn, T, inv_h, inv_h2);
+                        qi = first ? wi : __dadd_rn(wi, __dmul_rn(beta, qo));
+                    } else {
+                        qi = op_value<DIM, OP>(rc, di, vn, T, inv_h, inv_h2);
+                    }
                     dnew[i] = di;
                     q[i] = qi;
                     v1[0] = __dadd_rn(v1[0], __dmul_rn(di, qi));
                 }
                 // ghost-plane d, recomputed exactly as the owning slab computes it
+                // (QR reads neighbour z only)
+                if (!QR)
                 for (uint32_t i = m + tid; i < m_all; i += stride) {
                     double zc = z[i];
                     if (PROJ) zc = __dsub_rn(zc, mu);
@@ -182,9 +197,9 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
             };
             // peeling the first iteration pays for S_hat (B200, C2: 63.8 -> 57.3
             // us/it) but not for A (131.5 -> 137 us/it: register allocation)
-            if (OP == 1 && it == 0)
+            if (OP == 1 && !QR && it == 0)
                 pass1(std::true_type{});
-            else if (OP == 1)
+            else if (OP == 1 && !QR)
                 pass1(std::false_type{});
             else
                 pass1(it == 0);
@@ -578,6 +593,9 @@ static const void *cg1_fn_t(int tier) {
 template <int DIM, int OP>
 static const void *pcg_fn_t(int tier, int alg, int nt) {
     if (alg == CG_ONE_SUM) return nt == 512 ? cg1_fn_t<DIM, OP, 512>(tier) : cg1_fn_t<DIM, OP, CG_THREADS>(tier);
+    if (alg == CG_TWO_SUM_QREC)
+        return tier == 3 ? (const void *)k_pcg<DIM, OP, 3, true>
+                         : (tier == 2 ? (const void *)k_pcg<DIM, OP, 2, true> : (const void *)k_pcg<DIM, OP, 1, true>);
     return tier == 3 ? (const void *)k_pcg<DIM, OP, 3>
                      : (tier == 2 ? (const void *)k_pcg<DIM, OP, 2> : (const void *)k_pcg<DIM, OP, 1>);
 }

@@ -120,7 +120,9 @@ size_t cc_work_bytes(int64_t N);
 int64_t cc_label_device(const uint8_t *d_fluid, int dim, int n, int *d_labels, void *work, size_t work_bytes,
                         cudaStream_t s);
 constexpr size_t CG_SMEM_BUDGET = 200 * 1024;  // dynamic smem per block (1 block / SM)
-enum CgAlg { CG_TWO_SUM = 0, CG_ONE_SUM = 1 };  // k_pcg (reference order) | k_cg1 (one reduction)
+// k_pcg (reference order) | k_cg1 (one reduction) | k_pcg with q = A z + beta q_old
+// (value 3: 2 is the k_cg1t kernel id in vs_kstat)
+enum CgAlg { CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3 };
 struct CgPlan {
     int alg;
     int threads;  // block size of the launch
