@@ -188,10 +188,31 @@ def cli_cases():
     return out
 
 
+def spectra_cases():
+    """analyze_spectrum (both pencils) and nev_formula_check of the
+    reference on desk-scale packings (spectra.py:203-262)."""
+    from voxstokes.spectra import analyze_spectrum, nev_formula_check
+
+    out = {"analyze": [], "nev": []}
+    for prm in (dict(N=1, n_c=10, n_avg=4, n_min=2, seed=7),
+                dict(N=2, n_c=8, n_avg=4, n_min=2, seed=1),
+                dict(N=1, n_c=8, n_avg=4, n_min=2, seed=3, dim=3)):
+        grid = generate_packing(PackingParams(**prm))
+        for prec in ("none", "simple"):
+            rep = analyze_spectrum(grid, prec=prec)
+            out["analyze"].append({"params": prm, "prec": prec, "report": rep.to_json_dict(),
+                                   "eigenvalues": [float(v) for v in rep.eigenvalues]})
+    configs = [PackingParams(N=n, n_c=nc, n_avg=4, n_min=2, seed=0) for n in (1, 2) for nc in (8, 12)]
+    for row in nev_formula_check(configs, seeds=[0, 1]):
+        out["nev"].append({k: (bool(v) if isinstance(v, (bool, np.bool_)) else int(v))
+                           for k, v in row.items()})
+    return out
+
+
 def main():
     packing, rejected = packing_cases()
     doc = {"read": read_cases(), "packing": packing, "packing_rejected": rejected,
-           "cli": cli_cases()}
+           "cli": cli_cases(), "spectra": spectra_cases()}
     with open(os.path.join(HERE, "io_cases.json"), "w") as fh:
         json.dump(doc, fh, indent=1)
         fh.write("\n")

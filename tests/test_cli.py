@@ -75,13 +75,6 @@ def test_malformed_geometry_error(tmp_path, capsys):
     assert capsys.readouterr().err == "error: line 5, column 2: non-binary voxel symbol 'x'\n"
 
 
-def test_dense_subcommands_fail_cleanly(small_geom, capsys):
-    for cmd in ("spectrum", "nev-check"):
-        assert run_cli([cmd, str(small_geom)]) == 1
-        err = capsys.readouterr().err
-        assert err.startswith("error:") and err.count("\n") == 1
-
-
 def test_module_entry_point():
     env = dict(os.environ, PYTHONPATH=ROOT)
     proc = subprocess.run([sys.executable, "-m", "paper_2307_05266_b200", "stats", "missing.vox"],
