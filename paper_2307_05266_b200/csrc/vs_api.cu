@@ -572,6 +572,7 @@ void drain_log(vs_ctx *c, int from, int64_t *its_op) {
         st.dof_iters += o.iterations * m;
         st.ms += ms;
         st.kernel = c->use_tile[op] ? 2 : (op == 0 ? c->plan_A.alg : c->plan_S.alg);
+        st.reserved = op == 0 ? c->plan_A.unroll : c->plan_S.unroll;  // P1 DOFs per step
         if (its_op) its_op[li - from] = o.iterations;
         if (m) {
             Status s = cg_status_to_error(o, op);

@@ -34,7 +34,11 @@ namespace vs {
 // z only (6 loads instead of 12 in 3D) and reads its own q_old; neighbour d
 // is never needed, so the ghost-plane d recompute goes too.  Rounding
 // differs from q = A d at the last bits (not bitwise the reference's order).
-template <int DIM, int OP, int TIER, bool QR = false>
+// U (QR only): DOFs per step of P1's grid-stride loop; U = 2 issues both
+// DOFs' loads before either's arithmetic (twice the independent load chains
+// per thread).  The per-DOF arithmetic and the order of the d.q partial are
+// unchanged, so U = 1 and U = 2 give bitwise the same results.
+template <int DIM, int OP, int TIER, bool QR = false, int U = 1>
 __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
@@ -195,11 +199,60 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                     dnew[i] = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dold[i]));
                 }
             };
+            // P1 of the QR form: neighbour z only, U DOFs per step
+            auto pass1q = [&](bool first) {
+                uint32_t k = 0;
+                for (uint32_t i0 = tid; i0 < m; i0 += U * stride, k += U) {
+                    uint32_t ii[U], kk[U];
+                    bool ok[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {  // a DOF past the end repeats DOF 0 (not stored)
+                        ok[u] = (i0 + u * stride) < m;
+                        ii[u] = ok[u] ? i0 + u * stride : i0;
+                        kk[u] = ok[u] ? k + u : k;
+                    }
+                    double zc[U], dc[U], qo[U];
+                    uint64_t rc[U];
+                    uint32_t nr[U][NS];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        zc[u] = z[ii[u]];
+                        dc[u] = first ? 0.0 : dold[ii[u]];
+                        qo[u] = first ? 0.0 : q[ii[u]];
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) fetch_dof<DIM, OP, TIER>(P, G, cache, kk[u], kc, ii[u], rc[u], nr[u]);
+                    double zn[U][NS];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int s = 0; s < NS; ++s) zn[u][s] = z[nr[u][s] != ABSENT ? nr[u][s] : ii[u]];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (!ok[u]) break;
+                        const double zp = PROJ ? __dsub_rn(zc[u], mu) : zc[u];
+                        const double di = first ? zp : __dadd_rn(zp, __dmul_rn(beta, dc[u]));
+                        double vn[NS];
+#pragma unroll
+                        for (int s = 0; s < NS; ++s) {
+                            const double zj = PROJ ? __dsub_rn(zn[u][s], mu) : zn[u][s];
+                            vn[s] = (OP == 0 && nr[u][s] == ABSENT) ? 0.0 : zj;
+                        }
+                        const double wi = op_value<DIM, OP>(rc[u], zp, vn, T, inv_h, inv_h2);
+                        const double qi = first ? wi : __dadd_rn(wi, __dmul_rn(beta, qo[u]));
+                        dnew[ii[u]] = di;
+                        q[ii[u]] = qi;
+                        v1[0] = __dadd_rn(v1[0], __dmul_rn(di, qi));
+                    }
+                }
+            };
             // peeling the first iteration pays for S_hat (B200, C2: 63.8 -> 57.3
             // us/it) but not for A (131.5 -> 137 us/it: register allocation)
-            if (OP == 1 && !QR && it == 0)
+            if (QR)
+                pass1q(it == 0);
+            else if (OP == 1 && it == 0)
                 pass1(std::true_type{});
-            else if (OP == 1 && !QR)
+            else if (OP == 1)
                 pass1(std::false_type{});
             else
                 pass1(it == 0);
@@ -591,17 +644,18 @@ static const void *cg1_fn_t(int tier) {
                      : (tier == 2 ? (const void *)k_cg1<DIM, OP, 2, NT> : (const void *)k_cg1<DIM, OP, 1, NT>);
 }
 template <int DIM, int OP>
-static const void *pcg_fn_t(int tier, int alg, int nt) {
+static const void *pcg_fn_t(int tier, int alg, int nt, int u) {
     if (alg == CG_ONE_SUM) return nt == 512 ? cg1_fn_t<DIM, OP, 512>(tier) : cg1_fn_t<DIM, OP, CG_THREADS>(tier);
-    if (alg == CG_TWO_SUM_QREC)
+    if (alg == CG_TWO_SUM_QREC) {
         return tier == 3 ? (const void *)k_pcg<DIM, OP, 3, true>
                          : (tier == 2 ? (const void *)k_pcg<DIM, OP, 2, true> : (const void *)k_pcg<DIM, OP, 1, true>);
+    }
     return tier == 3 ? (const void *)k_pcg<DIM, OP, 3>
                      : (tier == 2 ? (const void *)k_pcg<DIM, OP, 2> : (const void *)k_pcg<DIM, OP, 1>);
 }
-static const void *pcg_fn(int dim, int op, int tier, int alg, int nt) {
-    if (dim == 3) return op == 0 ? pcg_fn_t<3, 0>(tier, alg, nt) : pcg_fn_t<3, 1>(tier, alg, nt);
-    return op == 0 ? pcg_fn_t<2, 0>(tier, alg, nt) : pcg_fn_t<2, 1>(tier, alg, nt);
+static const void *pcg_fn(int dim, int op, int tier, int alg, int nt, int u) {
+    if (dim == 3) return op == 0 ? pcg_fn_t<3, 0>(tier, alg, nt, u) : pcg_fn_t<3, 1>(tier, alg, nt, u);
+    return op == 0 ? pcg_fn_t<2, 0>(tier, alg, nt, u) : pcg_fn_t<2, 1>(tier, alg, nt, u);
 }
 
 // Plan one launch: blocks per group (all groups co-resident on one device),
@@ -609,6 +663,10 @@ static const void *pcg_fn(int dim, int op, int tier, int alg, int nt) {
 CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, bool nbr_tier, int sms) {
     CgPlan pl{};
     pl.alg = alg;
+    // P1 DOFs per step: 1.  (U = 2 -- both DOFs' loads issued first -- spills
+    // 100-156 B at 64 registers: B200 C2 A 124.7 -> 130.6, S_hat 59.0 -> 63.8
+    // us/it; the template keeps it for experiments.)
+    pl.unroll = 1;
     // k_cg1 on the projected S_hat runs 512-thread blocks (B200, C1: 7.2 -> 6.1
     // us/it: half the block-stage work in its 6-component grid sum); the A
     // solve and k_pcg keep 1024 (k_pcg at 512: C2 S_hat 57 -> 83 us/it)
@@ -622,7 +680,7 @@ CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, boo
     if (sms > 0 && sms < nsm) nsm = sms;  // a share of the device (concurrent solves)
     const int ns = 2 * dim;
     for (int tier : {2, nbr_tier ? 3 : 1}) {
-        const void *fn = pcg_fn(dim, op, tier, alg, nt);
+        const void *fn = pcg_fn(dim, op, tier, alg, nt, pl.unroll);
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, fn);  // static smem (grid_sum staging, tables)
         const size_t stage = alg == CG_ONE_SUM ? cg1_stage_bytes(op, nt) : 0;  // dynamic grid-sum staging
@@ -653,7 +711,7 @@ cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &
     P.cache_slots = pl.slots;
     P.bpg = pl.grid;
     void *args[] = {&P};
-    return cudaLaunchCooperativeKernel(pcg_fn(dim, op, pl.tier, pl.alg, pl.threads), dim3(pl.grid * groups), dim3(pl.threads), args,
+    return cudaLaunchCooperativeKernel(pcg_fn(dim, op, pl.tier, pl.alg, pl.threads, pl.unroll), dim3(pl.grid * groups), dim3(pl.threads), args,
                                        pl.smem, s);
 }
 

@@ -125,6 +125,7 @@ constexpr size_t CG_SMEM_BUDGET = 200 * 1024;  // dynamic smem per block (1 bloc
 enum CgAlg { CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3 };
 struct CgPlan {
     int alg;
+    int unroll;   // DOFs per P1 step (k_pcg<QR> only)
     int threads;  // block size of the launch
     int tier, grid;
     uint32_t slots;

@@ -6,6 +6,6 @@ for round in 1 2; do
   for spec in "$@"; do
     IFS='|' read -r label lib envs <<< "$spec"
     echo "== $label round $round"
-    env $envs VOXSCHUR_LIB=$(realpath $lib) python tools/prof_inner.py $cfg 1 --no-phases | grep solve
+    env $envs VOXSCHUR_LIB=$(realpath $lib) python tools/prof_inner.py $cfg 1 --no-phases | grep -- "-solve"
   done
 done
