@@ -472,11 +472,12 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         G.d0 = op == 0 ? S.u[U_D0] : S.p[P_SD0];
         G.d1 = op == 0 ? S.u[U_D1] : S.p[P_SD1];
         G.q = op == 0 ? S.u[U_CQ] : S.p[P_SQ];
-        if ((op == 0 ? c->plan_A : c->plan_S).tier == 3) {  // TIER 3 rank table, built on first use
+        const int tier = (op == 0 ? c->plan_A : c->plan_S).tier;
+        if (tier == 3 || tier == 4) {  // TIER 3 rank / TIER 4 delta table, built on first use
             uint32_t *&nb = S.nbr[op];
             if (!nb) {
                 nb = c->alloc<uint32_t>((size_t)2 * c->dim * std::max<int64_t>(1, S.m_own[op]));
-                launch_build_nbr(c->dim, op, G, c->n, c->nw, nb, c->stream);
+                launch_build_nbr(c->dim, op, G, c->n, c->nw, nb, c->stream, tier);
                 CK(cudaGetLastError());
             }
             G.nbr = nb;
@@ -854,9 +855,14 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
         return (op == 0 || m > kQrecS) ? (int)CG_TWO_SUM_QREC : (int)CG_TWO_SUM;
     };
     const char *en = getenv("VOXSCHUR_NBR");
-    const bool nbr = en && atoi(en) == 1 && R == 1;
+    // VOXSCHUR_NBR=1: TIER 3 (32-bit ranks), =2: TIER 4 (packed deltas)
+    const int nbr = (en && R == 1) ? (atoi(en) == 1 ? 3 : atoi(en) == 2 ? 4 : 0) : 0;
     C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max, 0), nbr, nsm);
-    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max, 1), nbr, nsm);
+    // Large S_hat solves read packed neighbour deltas (TIER 4) instead of the
+    // bitmask lookups (B200, C4 512^3: 794 -> 755 us/it; A-solves lose: C2
+    // 124 -> 128, C4 1588 -> 1628; C2 S_hat neutral).  VOXSCHUR_NBR=0 turns it off.
+    const int nbr_S = en ? nbr : (R == 1 && mp_max > kQrecS ? 4 : 0);
+    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max, 1), nbr_S, nsm);
     C->sms = nsm;
 }
 

@@ -629,9 +629,41 @@ __global__ void k_build_nbr(const CgGroup G, int n, int nw, uint32_t *out) {
 #pragma unroll
     for (int s = 0; s < 2 * DIM; ++s) out[(size_t)s * G.m_own + i] = nr[s];
 }
-void launch_build_nbr(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *out, cudaStream_t s) {
+// TIER 4 table: neighbour ranks as deltas from the DOF's own rank -- x+/x-
+// as int32 (always fit), y+/y- as int16; a DOF whose y-delta does not fit
+// or whose z-neighbour wraps is flagged (x.x = INT_MIN) for the bitmask
+// lookup.  Absent slots store 0 (the record's presence bits decide).
+template <int DIM, int OP>
+__global__ void k_build_dnb(const CgGroup G, int n, int nw, uint32_t *out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= G.m_own) return;
+    const uint64_t rc = G.rec[i];
+    uint32_t nr[2 * DIM];
+    neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), nw, n, G.nx, rc, i, nr);
+    auto delta = [&](int s) -> int64_t { return nr[s] == ABSENT ? 0 : (int64_t)nr[s] - (int64_t)i; };
+    bool flag = (nr[2 * DIM - 2] != ABSENT && nr[2 * DIM - 2] != i + 1) ||
+                (nr[2 * DIM - 1] != ABSENT && nr[2 * DIM - 1] != i - 1);
+    int2 dx = make_int2((int)delta(0), (int)delta(1));
+    if (DIM == 3) {
+        const int64_t a = delta(2), b = delta(3);
+        flag |= a < -32767 || a > 32767 || b < -32767 || b > 32767;
+        reinterpret_cast<short2 *>(out + 2 * (size_t)G.m_own)[i] = make_short2((short)a, (short)b);
+    }
+    if (flag) dx.x = INT_MIN;
+    reinterpret_cast<int2 *>(out)[i] = dx;
+}
+
+void launch_build_nbr(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *out, cudaStream_t s,
+                      int tier) {
     if (!G.m_own) return;
     const unsigned nb = (G.m_own + 255) / 256;
+    if (tier == 4) {
+        if (dim == 3)
+            op == 0 ? k_build_dnb<3, 0><<<nb, 256, 0, s>>>(G, n, nw, out) : k_build_dnb<3, 1><<<nb, 256, 0, s>>>(G, n, nw, out);
+        else
+            op == 0 ? k_build_dnb<2, 0><<<nb, 256, 0, s>>>(G, n, nw, out) : k_build_dnb<2, 1><<<nb, 256, 0, s>>>(G, n, nw, out);
+        return;
+    }
     if (dim == 3)
         op == 0 ? k_build_nbr<3, 0><<<nb, 256, 0, s>>>(G, n, nw, out) : k_build_nbr<3, 1><<<nb, 256, 0, s>>>(G, n, nw, out);
     else
@@ -646,6 +678,7 @@ static const void *cg1_fn_t(int tier) {
 template <int DIM, int OP>
 static const void *pcg_fn_t(int tier, int alg, int nt, int u) {
     if (alg == CG_ONE_SUM) return nt == 512 ? cg1_fn_t<DIM, OP, 512>(tier) : cg1_fn_t<DIM, OP, CG_THREADS>(tier);
+    if (tier == 4) return alg == CG_TWO_SUM_QREC ? (const void *)k_pcg<DIM, OP, 4, true> : (const void *)k_pcg<DIM, OP, 4>;
     if (alg == CG_TWO_SUM_QREC) {
         return tier == 3 ? (const void *)k_pcg<DIM, OP, 3, true>
                          : (tier == 2 ? (const void *)k_pcg<DIM, OP, 2, true> : (const void *)k_pcg<DIM, OP, 1, true>);
@@ -660,7 +693,7 @@ static const void *pcg_fn(int dim, int op, int tier, int alg, int nt, int u) {
 
 // Plan one launch: blocks per group (all groups co-resident on one device),
 // cache tier and slots, smem.  m = the largest owned DOF count of a group.
-CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, bool nbr_tier, int sms) {
+CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, int nbr_tier, int sms) {
     CgPlan pl{};
     pl.alg = alg;
     // P1 DOFs per step: 1.  (U = 2 -- both DOFs' loads issued first -- spills
@@ -679,7 +712,10 @@ CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, boo
     cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (sms > 0 && sms < nsm) nsm = sms;  // a share of the device (concurrent solves)
     const int ns = 2 * dim;
-    for (int tier : {2, nbr_tier ? 3 : 1}) {
+    // nbr_tier: 0 (bitmask lookups), 3 (32-bit ranks in HBM), 4 (packed deltas;
+    // k_pcg only)
+    const int alt = (nbr_tier == 3 || (nbr_tier == 4 && alg != CG_ONE_SUM)) ? nbr_tier : 1;
+    for (int tier : {2, alt}) {
         const void *fn = pcg_fn(dim, op, tier, alg, nt, pl.unroll);
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, fn);  // static smem (grid_sum staging, tables)

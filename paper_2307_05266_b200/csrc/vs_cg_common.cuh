@@ -3,6 +3,7 @@
 // bitmask meta, the bit-exact operator values, grid barrier and
 // deterministic grid sums, the block-resident DOF cache.
 #pragma once
+#include <climits>
 #include <cstdlib>
 #include <type_traits>
 
@@ -383,6 +384,39 @@ __device__ __forceinline__ void fetch_dof(const CgParams &P, const CgGroup &G, c
             __builtin_assume(__isGlobal(rec));
             rc = rec[i];
         }
+        return;
+    }
+    if (TIER == 4) {
+        // packed deltas: one 8-B and one 4-B coalesced load, issued before the
+        // record is needed; INT_MIN in x.x = wrap / out-of-range -> bitmask lookup
+        const int2 *xd = reinterpret_cast<const int2 *>(G.nbr);
+        __builtin_assume(__isGlobal(xd));
+        const int2 dx = __ldcs(xd + i);
+        short2 dy = make_short2(0, 0);
+        if (DIM == 3) {
+            const short2 *yd = reinterpret_cast<const short2 *>(G.nbr + 2 * (size_t)G.m_own);
+            __builtin_assume(__isGlobal(yd));
+            dy = __ldcs(yd + i);
+        }
+        if (k < kc) {
+            rc = C.rec[k * NT + threadIdx.x];
+        } else {
+            const uint64_t *rec = G.rec;
+            __builtin_assume(__isGlobal(rec));
+            rc = rec[i];
+        }
+        if (dx.x == INT_MIN) {
+            neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, i, nr);
+            return;
+        }
+        nr[0] = rec_has_nb<OP>(rc, 0) ? i + (uint32_t)dx.x : ABSENT;
+        nr[1] = rec_has_nb<OP>(rc, 1) ? i + (uint32_t)dx.y : ABSENT;
+        if (DIM == 3) {
+            nr[2] = rec_has_nb<OP>(rc, 2) ? i + (uint32_t)(int)dy.x : ABSENT;
+            nr[3] = rec_has_nb<OP>(rc, 3) ? i + (uint32_t)(int)dy.y : ABSENT;
+        }
+        nr[2 * DIM - 2] = rec_has_nb<OP>(rc, 2 * DIM - 2) ? i + 1 : ABSENT;
+        nr[2 * DIM - 1] = rec_has_nb<OP>(rc, 2 * DIM - 1) ? i - 1 : ABSENT;
         return;
     }
     if (k < kc) {

@@ -35,7 +35,8 @@ struct CgGroup {
     const double *rhs, *x0;
     double *x, *r, *z, *d0, *d1, *q;
     double *zb[2], *ub[2], *sb[2];  // k_cg1: double-buffered zr = M r, u = M A zr, s = M q
-    const uint32_t *nbr;            // TIER 3: neighbour ranks [2*dim][m_own] (ABSENT if none)
+    const uint32_t *nbr;            // TIER 3: neighbour ranks [2*dim][m_own] (ABSENT if none);
+                                    // TIER 4: int2 x-deltas [m_own], then short2 y-deltas [m_own] (3D)
     // halo: side s = 0 sends the first owned plane to the lower neighbour's
     // ghost_hi, s = 1 the last owned plane to the upper neighbour's ghost_lo;
     // per family f, local range [sbeg, send) -> zpeer[s][sdst + (i - sbeg)]
@@ -131,10 +132,11 @@ struct CgPlan {
     uint32_t slots;
     size_t smem;
 };
-CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, bool nbr_tier = false,
+CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, int nbr_tier = 0,
                 int sms = 0);
 // fill the TIER-3 neighbour-rank table of one group's owned DOFs
-void launch_build_nbr(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *out, cudaStream_t s);
+void launch_build_nbr(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *out, cudaStream_t s,
+                      int tier = 3);
 cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
 
 // ---- k_cg1t: plane-sweep tiles staged by TMA (vs_cgt.cu) ----------------
