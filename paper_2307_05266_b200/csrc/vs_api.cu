@@ -842,26 +842,30 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, C->device));
     if (sms > 0 && sms < nsm) nsm = sms;
     // Two-reduction loop: q by recurrence (k_pcg<QR>, 6 gathers per DOF
-    // instead of 12) for the A-solve at every size (B200: C2 132.5 -> 123.5,
-    // C4 512^3 1780 -> 1546 us/it) and for S_hat above kQrecS DOFs (C4 512^3
-    // 836 -> 804 us/it; at C2 it loses, 57.1 -> 60.0).  VOXSCHUR_CG=2 forces
-    // the reference-order q = A d everywhere, =3 the recurrence everywhere.
+    // instead of 12) for every A-solve (B200: C2 132.5 -> 123.5, C4 512^3
+    // 1780 -> 1546 us/it) and, with the packed neighbour deltas (TIER 4,
+    // below), for every single-slab S_hat solve (C2 57.3 -> 55.1, C4 512^3
+    // 836 -> 755 us/it).  Slab runs have no TIER 4; there S_hat takes the
+    // recurrence above kQrecS DOFs only (alone it loses at C2: 57.1 -> 58.2,
+    // wins at C4: 836 -> 784).  VOXSCHUR_CG=2 forces the reference-order
+    // q = A d everywhere, =3 the recurrence everywhere.
     constexpr int64_t kQrecS = 8 << 20;
     auto pick = [&](int64_t m, int op) {
         if (force == 3) return (int)CG_TWO_SUM_QREC;
         if (force == 2) return (int)CG_TWO_SUM;
         if (R == 1 && (force == 1 || (force == 0 && m <= (int64_t)4 * nsm * CG_THREADS)))
             return (int)CG_ONE_SUM;
-        return (op == 0 || m > kQrecS) ? (int)CG_TWO_SUM_QREC : (int)CG_TWO_SUM;
+        return (op == 0 || R == 1 || m > kQrecS) ? (int)CG_TWO_SUM_QREC : (int)CG_TWO_SUM;
     };
     const char *en = getenv("VOXSCHUR_NBR");
     // VOXSCHUR_NBR=1: TIER 3 (32-bit ranks), =2: TIER 4 (packed deltas)
     const int nbr = (en && R == 1) ? (atoi(en) == 1 ? 3 : atoi(en) == 2 ? 4 : 0) : 0;
     C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max, 0), nbr, nsm);
-    // Large S_hat solves read packed neighbour deltas (TIER 4) instead of the
-    // bitmask lookups (B200, C4 512^3: 794 -> 755 us/it; A-solves lose: C2
-    // 124 -> 128, C4 1588 -> 1628; C2 S_hat neutral).  VOXSCHUR_NBR=0 turns it off.
-    const int nbr_S = en ? nbr : (R == 1 && mp_max > kQrecS ? 4 : 0);
+    // Two-reduction S_hat solves read packed neighbour deltas (TIER 4) instead
+    // of the bitmask lookups (B200, with the recurrence: C2 58.2 -> 55.1, C4
+    // 512^3 794 -> 755 us/it; A-solves lose: C2 124 -> 128, C4 1588 -> 1628).
+    // VOXSCHUR_NBR=0 turns it off.  (Ignored by k_cg1.)
+    const int nbr_S = en ? nbr : (R == 1 ? 4 : 0);
     C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max, 1), nbr_S, nsm);
     C->sms = nsm;
 }
