@@ -374,6 +374,7 @@ int vs_grid_header(const char *path, int *dim, int64_t *n) {
     if (!f) return fail_os(errno);
     char buf[4096];
     size_t got = fread(buf, 1, sizeof buf, f);
+    long fsize = (fseek(f, 0, SEEK_END) == 0) ? ftell(f) : -1;
     fclose(f);
     std::string b(buf, got);
     // only the three header lines matter; drop a possibly cut fourth line
@@ -388,6 +389,10 @@ int vs_grid_header(const char *path, int *dim, int64_t *n) {
     if (int rc = parse_header(b, lines, &d, &n_canon)) return rc;
     int64_t nn = dec_small(n_canon);
     if (nn < 0 || nn > (int64_t(1) << 20)) return fail_value("size " + n_canon + " is out of range");
+    // a file too short for its data section: no buffer is sized from it (the
+    // full read reports the reference's size-mismatch error instead)
+    const int64_t rows = d == 2 ? nn : nn * nn;
+    if (fsize >= 0 && fsize < int64_t(nl) + rows * (nn + 1) - 1) return fail_value("file too short");
     *dim = d;
     *n = nn;
     return VS_OK;
@@ -414,7 +419,7 @@ int vs_read_grid(const char *path, uint8_t *fluid, int64_t cap, int *dim_out, in
     std::string n_canon;
     if (int rc = parse_header(b, head, &dim, &n_canon)) return rc;
     int64_t n = dec_small(n_canon);
-    int64_t E = (n < 0 || n > (int64_t(1) << 21)) ? -1 : (dim == 2 ? n : n * n);
+    int64_t E = (n < 0 || n > (int64_t(1) << 20)) ? -1 : (dim == 2 ? n : n * n);
     // fast path: E lines of n '0'/'1' each, then only '\n'
     bool ok = E > 0 && s <= b.size() && int64_t(b.size() - s) >= E * (n + 1) - 1;
     const size_t base = s;

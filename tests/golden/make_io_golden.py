@@ -75,6 +75,8 @@ def read_cases():
         "size_neg": H.encode() + b"dim 2\nsize -007\n",
         "size_double_underscore": H.encode() + b"dim 2\nsize 1__0\n",
         "size_huge": H.encode() + b"dim 3\nsize 123456789012345678901234\n0101\n",
+        "size_big_short": H.encode() + b"dim 3\nsize 1048576\n0101\n",
+        "size_short_2d": H.encode() + b"dim 2\nsize 3\n010\n",
         "too_few_lines": b"\n".join(lines3[:10]) + b"\n",
         "empty_data_line": b"\n".join(lines3[:5] + [b""] + lines3[6:]),
         "trailing_content": good3 + b"junk\n",
