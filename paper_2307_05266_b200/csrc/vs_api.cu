@@ -142,7 +142,11 @@ struct vs_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
     vs_kstat st_A{}, st_S{};  // stats of the last top-level call
     int64_t launches = 0;
-    uint32_t pf_dist = 0;  // L2 prefetch (measured neutral); VOXSCHUR_PREFETCH overrides
+    // L2 prefetch of k_pcg's own streams one grid stride ahead (B200, C4 512^3:
+    // S_hat 756 -> 652, A 1551 -> 1444 us/it; C2: A 123 -> 110; distance 2
+    // and 4 are worse); VOXSCHUR_PREFETCH overrides (0 = off)
+    uint32_t pf_dist = 1;
+    bool pf_forced = false;
 
     Geo geo() const {
         Geo g;
@@ -533,7 +537,9 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     memcpy(P.invA_enc, c->invA_enc, sizeof P.invA_enc);
     P.invS = c->invS;
     P.sdiag2 = c->sdiag2;
-    P.pf_dist = c->pf_dist;
+    // prefetch only where the operator's vectors leave L2 (C1 64^3, L2-resident,
+    // on a 46-SM share: A 7.6 -> 8.2 us/it with it); the env value applies as given
+    P.pf_dist = (c->pf_forced || m > (int64_t(1) << 20)) ? c->pf_dist : 0;
     const CgPlan &pl = op == 0 ? c->plan_A : c->plan_S;
     P.total_blocks = pl.grid * R;          // blocks of every rank
     P.block_base = pl.grid * c->s0;        // global index of this launch's block 0
@@ -1215,7 +1221,10 @@ static int create_common(const uint8_t *fluid, int dim, int n, int flow_dir, int
         C->sdiag_ok = hflag == 0;
         // ---- decomposition into x-slabs (1 = whole domain), work vectors, plans
         build_slabs(C, slabs, rank, nranks);
-        if (const char *pf = getenv("VOXSCHUR_PREFETCH")) C->pf_dist = (uint32_t)atoi(pf);
+        if (const char *pf = getenv("VOXSCHUR_PREFETCH")) {
+            C->pf_dist = (uint32_t)atoi(pf);
+            C->pf_forced = true;
+        }
         if (getenv("VOXSCHUR_PHASE_TIMING")) {
             C->phase_ns = C->alloc<unsigned long long>(12);
             CK(cudaMemsetAsync(C->phase_ns, 0, 12 * sizeof(unsigned long long), C->stream));

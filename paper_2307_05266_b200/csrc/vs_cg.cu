@@ -211,6 +211,19 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                         ii[u] = ok[u] ? i0 + u * stride : i0;
                         kk[u] = ok[u] ? k + u : k;
                     }
+                    const uint32_t ip = i0 + P.pf_dist * U * stride;
+                    if (P.pf_dist && ip < m) {  // the own streams pf_dist steps ahead (L2, no registers)
+                        prefetch_l2(z + ip);
+                        if (!first) {
+                            prefetch_l2(dold + ip);
+                            prefetch_l2(q + ip);
+                        }
+                        if (k + U * P.pf_dist >= kc) prefetch_l2(G.rec + ip);
+                        if (TIER == 4) {
+                            prefetch_l2(reinterpret_cast<const int2 *>(G.nbr) + ip);
+                            if (DIM == 3) prefetch_l2(reinterpret_cast<const short2 *>(G.nbr + 2 * (size_t)G.m_own) + ip);
+                        }
+                    }
                     double zc[U], dc[U], qo[U];
                     uint64_t rc[U];
                     uint32_t nr[U][NS];
