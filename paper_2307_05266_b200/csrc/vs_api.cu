@@ -866,12 +866,15 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     const char *en = getenv("VOXSCHUR_NBR");
     // VOXSCHUR_NBR=1: TIER 3 (32-bit ranks), =2: TIER 4 (packed deltas)
     const int nbr = (en && R == 1) ? (atoi(en) == 1 ? 3 : atoi(en) == 2 ? 4 : 0) : 0;
-    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max, 0), nbr, nsm);
-    // Two-reduction S_hat solves read packed neighbour deltas (TIER 4) instead
-    // of the bitmask lookups (B200, with the recurrence: C2 58.2 -> 55.1, C4
-    // 512^3 794 -> 755 us/it; A-solves lose: C2 124 -> 128, C4 1588 -> 1628).
+    // Two-reduction solves on one slab read packed neighbour deltas (TIER 4)
+    // instead of the bitmask lookups when the ranks do not fit the smem DOF
+    // cache (B200, with the recurrence: S_hat C2 58.2 -> 55.1, C4 512^3 794 ->
+    // 755 us/it; A-solves gain only together with the carried delta words
+    // and the L2 prefetch: C2 110.9 -> 102.7, C4 1448 -> 1371).
     // VOXSCHUR_NBR=0 turns it off.  (Ignored by k_cg1.)
-    const int nbr_S = en ? nbr : (R == 1 ? 4 : 0);
+    const int nbr_A = en ? nbr : (R == 1 ? 4 : 0);
+    const int nbr_S = nbr_A;
+    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max, 0), nbr_A, nsm);
     C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max, 1), nbr_S, nsm);
     C->sms = nsm;
 }

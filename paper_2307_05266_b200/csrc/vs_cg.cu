@@ -38,8 +38,9 @@ namespace vs {
 // DOFs' loads before either's arithmetic (twice the independent load chains
 // per thread).  The per-DOF arithmetic and the order of the d.q partial are
 // unchanged, so U = 1 and U = 2 give bitwise the same results.
-template <int DIM, int OP, int TIER, bool QR = false, int U = 1>
+template <int DIM, int OP, int TIER, bool QR = false, int U_ = 1>
 __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
+    constexpr int U = U_ > 0 ? U_ : 1;  // U_ == 0: P1 with carried delta words (TIER 4)
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
     extern __shared__ __align__(16) uint8_t dyn_smem[];
@@ -259,9 +260,81 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
                     }
                 }
             };
+            // P1 of the QR form at TIER 4 with the next DOF's delta words and
+            // record carried across the step (U == 0): the rank decode of a step
+            // waits on nothing, and the gathers issue with the own loads
+            auto pass1c = [&](bool first) {
+                const int2 *xd = reinterpret_cast<const int2 *>(G.nbr);
+                const short2 *yd = reinterpret_cast<const short2 *>(G.nbr + 2 * (size_t)G.m_own);
+                __builtin_assume(__isGlobal(xd));
+                __builtin_assume(__isGlobal(yd));
+                const uint64_t *rec = G.rec;
+                __builtin_assume(__isGlobal(rec));
+                int2 dxn = make_int2(0, 0);
+                short2 dyn = make_short2(0, 0);
+                uint64_t rcn = 0;
+                auto words = [&](uint32_t i, uint32_t kk) {
+                    dxn = __ldcs(xd + i);
+                    if (DIM == 3) dyn = __ldcs(yd + i);
+                    rcn = kk < kc ? cache.rec[kk * CG_THREADS + threadIdx.x] : rec[i];
+                };
+                if (tid < m) words(tid, 0);
+                uint32_t k = 0;
+                for (uint32_t i = tid; i < m; i += stride, ++k) {
+                    const uint32_t ip = i + P.pf_dist * stride;
+                    if (P.pf_dist && ip < m) {
+                        prefetch_l2(z + ip);
+                        if (!first) {
+                            prefetch_l2(dold + ip);
+                            prefetch_l2(q + ip);
+                        }
+                        if (k + P.pf_dist >= kc) prefetch_l2(rec + ip);
+                        prefetch_l2(xd + ip);
+                        if (DIM == 3) prefetch_l2(yd + ip);
+                    }
+                    const int2 dx = dxn;
+                    const short2 dy = dyn;
+                    const uint64_t rc = rcn;
+                    const double zc = z[i];
+                    const double dc = first ? 0.0 : dold[i];
+                    const double qo = first ? 0.0 : q[i];
+                    uint32_t nr[NS];
+                    if (dx.x == INT_MIN) {
+                        neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, i, nr);
+                    } else {
+                        nr[0] = rec_has_nb<OP>(rc, 0) ? i + (uint32_t)dx.x : ABSENT;
+                        nr[1] = rec_has_nb<OP>(rc, 1) ? i + (uint32_t)dx.y : ABSENT;
+                        if (DIM == 3) {
+                            nr[2] = rec_has_nb<OP>(rc, 2) ? i + (uint32_t)(int)dy.x : ABSENT;
+                            nr[3] = rec_has_nb<OP>(rc, 3) ? i + (uint32_t)(int)dy.y : ABSENT;
+                        }
+                        nr[NS - 2] = rec_has_nb<OP>(rc, NS - 2) ? i + 1 : ABSENT;
+                        nr[NS - 1] = rec_has_nb<OP>(rc, NS - 1) ? i - 1 : ABSENT;
+                    }
+                    double zn[NS];
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) zn[s] = z[nr[s] != ABSENT ? nr[s] : i];
+                    if (i + stride < m) words(i + stride, k + 1);
+                    const double zp = PROJ ? __dsub_rn(zc, mu) : zc;
+                    const double di = first ? zp : __dadd_rn(zp, __dmul_rn(beta, dc));
+                    double vn[NS];
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) {
+                        const double zj = PROJ ? __dsub_rn(zn[s], mu) : zn[s];
+                        vn[s] = (OP == 0 && nr[s] == ABSENT) ? 0.0 : zj;
+                    }
+                    const double wi = op_value<DIM, OP>(rc, zp, vn, T, inv_h, inv_h2);
+                    const double qi = first ? wi : __dadd_rn(wi, __dmul_rn(beta, qo));
+                    dnew[i] = di;
+                    q[i] = qi;
+                    v1[0] = __dadd_rn(v1[0], __dmul_rn(di, qi));
+                }
+            };
             // peeling the first iteration pays for S_hat (B200, C2: 63.8 -> 57.3
             // us/it) but not for A (131.5 -> 137 us/it: register allocation)
-            if (QR)
+            if (QR && U_ == 0 && TIER == 4)
+                pass1c(it == 0);
+            else if (QR)
                 pass1q(it == 0);
             else if (OP == 1 && it == 0)
                 pass1(std::true_type{});
@@ -691,7 +764,9 @@ static const void *cg1_fn_t(int tier) {
 template <int DIM, int OP>
 static const void *pcg_fn_t(int tier, int alg, int nt, int u) {
     if (alg == CG_ONE_SUM) return nt == 512 ? cg1_fn_t<DIM, OP, 512>(tier) : cg1_fn_t<DIM, OP, CG_THREADS>(tier);
-    if (tier == 4) return alg == CG_TWO_SUM_QREC ? (const void *)k_pcg<DIM, OP, 4, true> : (const void *)k_pcg<DIM, OP, 4>;
+    if (tier == 4)
+        return alg == CG_TWO_SUM_QREC ? (u == 0 ? (const void *)k_pcg<DIM, OP, 4, true, 0> : (const void *)k_pcg<DIM, OP, 4, true>)
+                                      : (const void *)k_pcg<DIM, OP, 4>;
     if (alg == CG_TWO_SUM_QREC) {
         return tier == 3 ? (const void *)k_pcg<DIM, OP, 3, true>
                          : (tier == 2 ? (const void *)k_pcg<DIM, OP, 2, true> : (const void *)k_pcg<DIM, OP, 1, true>);
@@ -713,6 +788,13 @@ CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, int
     // 100-156 B at 64 registers: B200 C2 A 124.7 -> 130.6, S_hat 59.0 -> 63.8
     // us/it; the template keeps it for experiments.)
     pl.unroll = 1;
+    // k_pcg_qrec at TIER 4 carries the next DOF's delta words across the P1
+    // step (unroll 0; B200: C2 S_hat 56.3 -> 53.5, C4 512^3 651 -> 634 us/it,
+    // despite 56-88 B of spills); VOXSCHUR_P1CARRY=0 turns it off
+    if (alg == CG_TWO_SUM_QREC) {
+        const char *e = getenv("VOXSCHUR_P1CARRY");
+        if (!e || atoi(e) == 1) pl.unroll = 0;
+    }
     // k_cg1 on the projected S_hat runs 512-thread blocks (B200, C1: 7.2 -> 6.1
     // us/it: half the block-stage work in its 6-component grid sum); the A
     // solve and k_pcg keep 1024 (k_pcg at 512: C2 S_hat 57 -> 83 us/it)
