@@ -480,7 +480,9 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         if (tier == 3 || tier == 4) {  // TIER 3 rank / TIER 4 delta table, built on first use
             uint32_t *&nb = S.nbr[op];
             if (!nb) {
-                nb = c->alloc<uint32_t>((size_t)2 * c->dim * std::max<int64_t>(1, S.m_own[op]));
+                // TIER 3: 2*dim ranks; TIER 4: int2 x-deltas (+ short2 y-deltas in 3D)
+                const size_t words = tier == 4 ? (c->dim == 3 ? 3 : 2) : 2 * c->dim;
+                nb = c->alloc<uint32_t>(words * std::max<int64_t>(1, S.m_own[op]));
                 launch_build_nbr(c->dim, op, G, c->n, c->nw, nb, c->stream, tier);
                 CK(cudaGetLastError());
             }
