@@ -850,31 +850,29 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, C->device));
     if (sms > 0 && sms < nsm) nsm = sms;
     // Two-reduction loop: q by recurrence (k_pcg<QR>, 6 gathers per DOF
-    // instead of 12) for every A-solve (B200: C2 132.5 -> 123.5, C4 512^3
-    // 1780 -> 1546 us/it) and, with the packed neighbour deltas (TIER 4,
-    // below), for every single-slab S_hat solve (C2 57.3 -> 55.1, C4 512^3
-    // 836 -> 755 us/it).  Slab runs have no TIER 4; there S_hat takes the
-    // recurrence above kQrecS DOFs only (alone it loses at C2: 57.1 -> 58.2,
-    // wins at C4: 836 -> 784).  VOXSCHUR_CG=2 forces the reference-order
-    // q = A d everywhere, =3 the recurrence everywhere.
-    constexpr int64_t kQrecS = 8 << 20;
+    // instead of 12) for every A- and S_hat-solve, with the packed neighbour
+    // deltas (TIER 4, below) -- single slab and slab groups alike (B200, C2:
+    // A 132.5 -> 97, S_hat 57.3 -> 53.5; C4 512^3: A 1780 -> 1438, S_hat 836
+    // -> 641 us/it, with the carried delta words and the L2 prefetch; C2 on
+    // 1/2/4 slab groups: A 96.8/99.1/99.6, S_hat 53.5/53.4/54.4).
+    // VOXSCHUR_CG=2 forces the reference-order q = A d, =3 the recurrence.
     auto pick = [&](int64_t m, int op) {
         if (force == 3) return (int)CG_TWO_SUM_QREC;
         if (force == 2) return (int)CG_TWO_SUM;
         if (R == 1 && (force == 1 || (force == 0 && m <= (int64_t)4 * nsm * CG_THREADS)))
             return (int)CG_ONE_SUM;
-        return (op == 0 || R == 1 || m > kQrecS) ? (int)CG_TWO_SUM_QREC : (int)CG_TWO_SUM;
+        return (int)CG_TWO_SUM_QREC;
     };
     const char *en = getenv("VOXSCHUR_NBR");
     // VOXSCHUR_NBR=1: TIER 3 (32-bit ranks), =2: TIER 4 (packed deltas)
-    const int nbr = (en && R == 1) ? (atoi(en) == 1 ? 3 : atoi(en) == 2 ? 4 : 0) : 0;
+    const int nbr = en ? (atoi(en) == 1 && R == 1 ? 3 : atoi(en) == 2 ? 4 : 0) : 0;
     // Two-reduction solves on one slab read packed neighbour deltas (TIER 4)
     // instead of the bitmask lookups when the ranks do not fit the smem DOF
     // cache (B200, with the recurrence: S_hat C2 58.2 -> 55.1, C4 512^3 794 ->
     // 755 us/it; A-solves gain only together with the carried delta words
     // and the L2 prefetch: C2 110.9 -> 102.7, C4 1448 -> 1371).
     // VOXSCHUR_NBR=0 turns it off.  (Ignored by k_cg1.)
-    const int nbr_A = en ? nbr : (R == 1 ? 4 : 0);
+    const int nbr_A = en ? nbr : 4;
     const int nbr_S = nbr_A;
     C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max, 0), nbr_A, nsm);
     C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max, 1), nbr_S, nsm);
