@@ -82,6 +82,14 @@ int vs_components(const uint8_t *fluid, int dim, int n, int32_t *labels,
 int vs_components_device(const uint8_t *fluid, int dim, int n, int device, int32_t *labels,
                          int64_t *n_components);
 
+/* Percolation along `axis` on the periodic box: a component percolates iff it
+ * holds a closed path of non-zero winding along that axis.  Union-find over
+ * the fluid cells carrying the unwrapped axis offset (the periodic merge of
+ * geometry.py:183-222 extended as SURVEY App. B-3 asks; host C++).  Returns
+ * the number of periodic components and how many of them wind. */
+int vs_winding(const uint8_t *fluid, int dim, int n, int axis, int64_t *n_components,
+               int64_t *n_winding);
+
 /* voxgeo text IO (geometry.py:243-339), multithreaded host C++.
  * vs_grid_header: dim and size from the three header lines only (to size
  * the caller's buffer); vs_read_grid: the whole file with the reference's
@@ -203,6 +211,11 @@ typedef struct {
                              iteration, reference operation order), 1 k_cg1
                              (one grid sum), 2 k_cg1t (one grid sum, tiled) */
     int32_t reserved;
+    int32_t tier;         /* where the fused CG took its neighbour ranks from:
+                             1 bitmask lookups (records smem-cached), 2 ranks in
+                             the smem DOF cache, 3 32-bit ranks streamed from
+                             HBM, 4 packed deltas streamed from HBM */
+    int32_t _pad;
 } vs_kstat;
 
 int vs_kernel_stats(vs_ctx *ctx, vs_kstat *velocity_cg, vs_kstat *simple_cg,

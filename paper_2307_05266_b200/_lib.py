@@ -52,6 +52,8 @@ class VsKstat(C.Structure):
         ("ms", C.c_double),
         ("kernel", C.c_int32),
         ("reserved", C.c_int32),
+        ("tier", C.c_int32),
+        ("_pad", C.c_int32),
     ]
 
 
@@ -75,6 +77,7 @@ def _load():
         "vs_version": (C.c_char_p, []),
         "vs_components": (C.c_int, [u8, C.c_int, C.c_int, P, i64p]),
         "vs_components_device": (C.c_int, [u8, C.c_int, C.c_int, C.c_int, P, i64p]),
+        "vs_winding": (C.c_int, [u8, C.c_int, C.c_int, C.c_int, i64p, i64p]),
         "vs_stamp_balls": (C.c_int, [P, C.c_int, C.c_int, P, P, C.c_int64, C.c_int64, C.c_int,
                                      i64p, i64p]),
         "vs_ctx_create": (C.c_int, [u8, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -118,7 +121,7 @@ def _load():
 
 lib = _load()
 EXPORTED = (
-    "vs_last_error", "vs_version", "vs_components", "vs_components_device", "vs_stamp_balls", "vs_ctx_create", "vs_ctx_create2", "vs_slab_count", "vs_ctx_limit_sms", "vs_ctx_sms", "vs_solve_span_ms", "vs_slab_plan", "vs_ctx_create_rank", "vs_ipc_handle", "vs_ipc_attach",
+    "vs_last_error", "vs_version", "vs_components", "vs_components_device", "vs_winding", "vs_stamp_balls", "vs_ctx_create", "vs_ctx_create2", "vs_slab_count", "vs_ctx_limit_sms", "vs_ctx_sms", "vs_solve_span_ms", "vs_slab_plan", "vs_ctx_create_rank", "vs_ipc_handle", "vs_ipc_attach",
     "vs_ctx_destroy",
     "vs_counts", "vs_export_geometry", "vs_apply_laplacian", "vs_apply_divergence",
     "vs_apply_gradient", "vs_divergence_weighted_diagonal", "vs_apply_simple",

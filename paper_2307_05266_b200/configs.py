@@ -14,8 +14,14 @@ module defines them once, deterministically:
   vs_stamp_balls), or exactly ``count`` balls when a count is given.
 * "Fluid = connected component percolating in x": keep the largest
   periodic component (the reference's enforce_connectivity rule,
-  geometry.py:225-240) and assert it reaches every x-plane; generation
-  fails loudly otherwise (the seed is never silently changed).
+  geometry.py:225-240) and assert that it percolates in x -- that it holds a
+  closed path of non-zero x-winding (``winding``: the periodic union-find of
+  geometry.py:183-222 carrying the unwrapped x-offset, SURVEY App. B-3);
+  generation fails loudly otherwise (the seed is never silently changed).
+* Slits and x-cylinders are x-prismatic: every fluid component percolates
+  in x, so all of them are kept (``check_connectivity=False`` at assemble,
+  as the reference needs for multi-component masks, operators.py:224-230)
+  and the winding check asserts exactly that.
 """
 from __future__ import annotations
 
@@ -27,7 +33,7 @@ import numpy as np
 from . import _lib
 from .geometry import VoxelGrid, enforce_connectivity
 
-__all__ = ["ConfigSpec", "CONFIGS", "make_geometry", "balls", "slits", "x_percolates"]
+__all__ = ["ConfigSpec", "CONFIGS", "make_geometry", "balls", "slits", "winding", "x_percolates"]
 
 BATCH = 4096
 
@@ -73,9 +79,23 @@ def slits(n: int, w: int, wall: int = 4) -> np.ndarray:
     return fluid
 
 
+def winding(fluid: np.ndarray, axis: int = 0) -> tuple[int, int]:
+    """(periodic components, components that percolate along ``axis``).
+
+    A component percolates iff it contains a closed path whose unwrapped
+    displacement along ``axis`` is a non-zero multiple of n (vs_winding:
+    union-find over the fluid cells that carries the axis offset)."""
+    f = np.ascontiguousarray(fluid, dtype=np.uint8)
+    nc, nw = C.c_int64(), C.c_int64()
+    _lib.check(_lib.lib.vs_winding(f.reshape(-1), f.ndim, f.shape[0], int(axis),
+                                   C.byref(nc), C.byref(nw)))
+    return int(nc.value), int(nw.value)
+
+
 def x_percolates(fluid: np.ndarray) -> bool:
-    """Necessary condition for x-percolation: every x-plane holds fluid."""
-    return bool(fluid.reshape(fluid.shape[0], -1).any(axis=1).all())
+    """True when every periodic fluid component of the mask percolates in x."""
+    nc, nw = winding(fluid, 0)
+    return nc > 0 and nc == nw
 
 
 @dataclass(frozen=True)
@@ -99,7 +119,8 @@ CONFIGS = {
     "C1": ConfigSpec("C1 64^3 spheres phi0.4", 64, 3, "balls", 4, 8, porosity=0.4),
     "C2": ConfigSpec("C2 256^3 spheres phi0.15", 256, 3, "balls", 2, 4, porosity=0.15,
                      precs=("simple", "uzawa")),
-    "C3c": ConfigSpec("C3 256^3 x-cylinders r3 phi0.3", 256, 3, "cylinders", 3, 3, porosity=0.3),
+    "C3c": ConfigSpec("C3 256^3 x-cylinders r3 phi0.3", 256, 3, "cylinders", 3, 3, porosity=0.3,
+                      check_connectivity=False),
     "C4": ConfigSpec("C4 512^3 spheres phi0.2", 512, 3, "balls", 3, 6, porosity=0.2,
                      precs=("simple",)),
     "C4L": ConfigSpec("C4 1024^3 spheres phi0.2", 1024, 3, "balls", 3, 6, porosity=0.2,
@@ -116,14 +137,17 @@ def make_geometry(key: str, seed: int = 0, n: int | None = None, device: int | N
     spec = CONFIGS[key]
     n = spec.n if n is None else n
     if spec.kind == "slits":
-        return VoxelGrid(slits(n, spec.width))
-    if spec.kind == "cylinders":
-        fluid = balls(n, spec.dim, spec.rmin, spec.rmax, porosity=spec.porosity, seed=seed,
-                      prism_axis=0)
+        grid = VoxelGrid(slits(n, spec.width))
+    elif spec.kind == "cylinders":
+        # x-prisms: every fluid component percolates in x, so all are kept
+        grid = VoxelGrid(balls(n, spec.dim, spec.rmin, spec.rmax, porosity=spec.porosity, seed=seed,
+                               prism_axis=0))
     else:
         fluid = balls(n, spec.dim, spec.rmin, spec.rmax, porosity=spec.porosity,
                       count=spec.count, seed=seed)
-    grid, _ = enforce_connectivity(VoxelGrid(fluid), device)
-    if not x_percolates(grid.fluid):
-        raise ValueError(f"{key} seed {seed}: kept component does not reach every x-plane")
+        grid, _ = enforce_connectivity(VoxelGrid(fluid), device)
+    nc, nw = winding(grid.fluid, 0)
+    if nc == 0 or nw != nc:
+        raise ValueError(f"{key} seed {seed}: {nc - nw} of {nc} kept fluid components do not "
+                         "percolate in x")
     return grid

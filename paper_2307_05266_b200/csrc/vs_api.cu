@@ -531,6 +531,11 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.out = c->cglog + li;
     P.tol = eps;
     P.max_iter = std::max<int64_t>(1000, 2 * m);  // schur.py:196-197
+    // test hook: a lower cap, to drive the "did not converge" paths of
+    // schur.py:214-218 / :266-271 (the reference's cap cannot be reached on
+    // an SPD operator in exact arithmetic)
+    if (const char *e = getenv("VOXSCHUR_INNER_MAXIT"))
+        if (atoll(e) > 0) P.max_iter = std::min<int64_t>(P.max_iter, atoll(e));
     P.norm_prec = 1;
     P.inv_h = c->inv_h;
     P.inv_h2 = c->inv_h2;
@@ -582,6 +587,7 @@ void drain_log(vs_ctx *c, int from, int64_t *its_op) {
         st.ms += ms;
         st.kernel = c->use_tile[op] ? 2 : (op == 0 ? c->plan_A.alg : c->plan_S.alg);
         st.reserved = op == 0 ? c->plan_A.unroll : c->plan_S.unroll;  // P1 DOFs per step
+        st.tier = op == 0 ? c->plan_A.tier : c->plan_S.tier;
         if (its_op) its_op[li - from] = o.iterations;
         if (m) {
             Status s = cg_status_to_error(o, op);
@@ -1079,6 +1085,11 @@ static int create_common(const uint8_t *fluid, int dim, int n, int flow_dir, int
     if (dim != 2 && dim != 3) return fail(VS_EVALUE, "grid dimension must be 2 or 3, got %d", dim);
     if (n < 2) return fail(VS_EVALUE, "grid extent must be at least 2, got %d", n);
     if (n > 2047) return fail(VS_EVALUE, "grid extent %d exceeds the record layout limit 2047", n);
+    // cell indices, component labels and the meta prefix counts are 32-bit
+    // (3D: n <= 1290); a larger grid must be decomposed before it gets here
+    if ((dim == 3 ? (int64_t)n * n * n : (int64_t)n * n) >= ((int64_t)1 << 31))
+        return fail(VS_EVALUE, "grid of %lld cells exceeds the 32-bit cell index (n <= 1290 in 3D)",
+                    (long long)(dim == 3 ? (int64_t)n * n * n : (int64_t)n * n));
     if (flow_dir < 0 || flow_dir >= dim) return fail(VS_EVALUE, "flow axis %d out of range for dim %d", flow_dir, dim);
     if (slabs < 1 || slabs > VS_MAX_SLABS || slabs > n)
         return fail(VS_EVALUE, "slab count %d out of range [1, min(%d, n)]", slabs, VS_MAX_SLABS);

@@ -189,3 +189,80 @@ def test_stamp_balls_matches_rule(dim, n, prism):
     if nf1 > target:
         u2, nf1 = configs._stamp(fl2, c[half:], r[half:], target, prism, nf1)
     assert nf1 == nf_ref and np.array_equal(fl2.astype(bool), ref)
+
+
+@pytest.mark.parametrize("key,n", [("C0", None), ("C1", None), ("C2", 96), ("C3c", 64), ("C3s8", 64), ("C4", 96)])
+def test_config_generator_matches_oracle_stamper(key, n):
+    """The product generator (native stamper + enforce_connectivity) and the
+    pure-numpy generator the reference fixtures were made with give the same
+    mask, bit for bit."""
+    from oracle import stamper
+    from paper_2307_05266_b200 import configs
+
+    a = configs.make_geometry(key, 0, n).fluid
+    b = stamper.make_fluid(key, 0, n)
+    assert a.shape == b.shape and np.array_equal(a, b)
+    assert stamper.mask_digest(a) == stamper.mask_digest(b)
+
+
+def test_winding_known_cases():
+    """x-percolation = a closed fluid path of non-zero x-winding."""
+    from paper_2307_05266_b200 import configs
+
+    n = 8
+    f = np.zeros((n, n), bool)
+    f[:, 3] = True                                   # straight channel along x
+    assert configs.winding(f, 0) == (1, 1) and configs.winding(f, 1) == (1, 0)
+    f = np.zeros((n, n), bool)
+    f[2:6, 2:6] = True                               # a blob reaches nothing
+    assert configs.winding(f, 0) == (1, 0) and not configs.x_percolates(f)
+    # a plug of fluid in every x-plane that never connects: the old "every
+    # x-plane holds fluid" test passes it, the winding test does not
+    f = np.zeros((n, n), bool)
+    f[::2, 1] = True
+    f[1::2, 5] = True
+    assert f.any(axis=1).all() and configs.winding(f, 0) == (n, 0)
+    # a diagonal channel that advances n/2 in y per x-period: open when alone,
+    # closed (winding 2) when its half-period partner is there too
+    one, two = np.zeros((n, n), bool), np.zeros((n, n), bool)
+    for x in range(n):
+        y = x // 2
+        one[x, [y, (y + 1) % n]] = True
+        two[x, [y, (y + 1) % n, (y + 4) % n, (y + 5) % n]] = True
+    assert configs.winding(one, 0) == (1, 0)
+    assert configs.winding(two, 0) == (1, 1)
+    # 3D: a helix around x built from unit steps
+    f = np.zeros((6, 6, 6), bool)
+    f[:, 2, 2] = True
+    f[3, 2, 2] = False                               # cut it ...
+    assert configs.winding(f, 0) == (1, 0)
+    f[3, 3, 2] = f[2, 3, 2] = f[4, 3, 2] = True      # ... and bridge the cut sideways
+    assert configs.winding(f, 0) == (1, 1)
+    # n = 2: the +x and -x neighbours coincide; a full line still wraps
+    f = np.ones((2, 2), bool)
+    assert configs.winding(f, 0) == (1, 1)
+
+
+def test_cylinders_keep_every_component():
+    """C3 cylinders are x-prisms: all components percolate and all are kept
+    (porosity stays at the BASELINE value instead of the largest component's)."""
+    from paper_2307_05266_b200 import configs
+
+    g = configs.make_geometry("C3c", 0, 64)
+    nc, nw = configs.winding(g.fluid, 0)
+    assert nc > 1 and nw == nc
+    assert abs(g.fluid.mean() - 0.3) < 0.01
+    assert not configs.CONFIGS["C3c"].check_connectivity
+
+
+def test_grid_too_large_for_32bit_cells():
+    """assemble rejects a 3D grid of >= 2^31 cells before any device work
+    (cell indices and labels are 32-bit); checked on a mask that is never
+    allocated in full: the size check comes first."""
+    import ctypes as C
+    from paper_2307_05266_b200 import _lib
+
+    ctx = C.c_void_p()
+    tiny = np.ones(8, dtype=np.uint8)
+    rc = _lib.lib.vs_ctx_create(tiny, 3, 1291, 0, 1, 1, 0, 1291.0, 1291.0 ** 2, C.byref(ctx))
+    assert rc == _lib.VS_EVALUE and b"32-bit cell index" in _lib.lib.vs_last_error()
