@@ -198,6 +198,22 @@ int vs_solve_schur(vs_ctx *ctx, const vs_schur_cfg *cfg, double *pressure,
                    double *res_unprec, double *perm_history, double *alpha,
                    double *beta);
 
+/* The same outer PCG on S with the caller's right-hand side g (m_p values)
+ * in place of B A^-1 f -- i.e. krylov.py:76 pcg(outer_op, outer_prec, g) with
+ * the operator and preconditioner closures of schur.py:312-327.  For the
+ * flow-aligned prismatic C3 geometries g = B A^-1 f is exactly 0, the
+ * reference does 0 outer iterations and reports no Lanczos estimate
+ * (schur.py:359-362); SURVEY App. B-4 asks for a labelled supplementary
+ * estimate from a seeded zero-mean g.  alpha/beta are the CG coefficients
+ * lanczos_condition_estimate (krylov.py:185-205) takes.  pressure receives
+ * the solution S^-1 g; velocity / perm_history / k_value follow the same
+ * code path (u_f + sum alpha w, then the refresh) and carry no physical
+ * meaning for an arbitrary g. */
+int vs_solve_schur_rhs(vs_ctx *ctx, const vs_schur_cfg *cfg, const double *g,
+                       double *pressure, double *velocity, vs_report *rep,
+                       double *res_prec, double *res_unprec, double *perm_history,
+                       double *alpha, double *beta);
+
 /* Bench hooks: CUDA-event timing of the fused persistent CG launches of the
  * most recent vs_solve_schur / inner solve, split by operator.  dof_iters =
  * sum over launches of (iterations x vector length); launches counts kernel

