@@ -225,13 +225,18 @@ typedef struct {
     double ms;            /* summed CUDA-event duration of the launches */
     int32_t kernel;       /* which fused CG ran: 0 k_pcg (two grid sums per
                              iteration, reference operation order), 1 k_cg1
-                             (one grid sum), 2 k_cg1t (one grid sum, tiled) */
+                             (one grid sum), 2 k_cg1t (one grid sum, tiled), 3 k_pcg
+                             with q by recurrence, 4 / 5 k_pcgm (M-scaled over 8-B
+                             descriptors; s = M q by recurrence / q recomputed) */
     int32_t reserved;
     int32_t tier;         /* where the fused CG took its neighbour ranks from:
                              1 bitmask lookups (records smem-cached), 2 ranks in
                              the smem DOF cache, 3 32-bit ranks streamed from
-                             HBM, 4 packed deltas streamed from HBM */
-    int32_t _pad;
+                             HBM, 4 packed deltas streamed from HBM, 5 8-B
+                             descriptors streamed from HBM (k_pcgm) */
+    int32_t escape_ppm;   /* k_pcgm (tier 5, 8-B descriptors): DOFs per million whose
+                             neighbour deltas do not fit the descriptor and take the
+                             record + bitmask lookup */
 } vs_kstat;
 
 int vs_kernel_stats(vs_ctx *ctx, vs_kstat *velocity_cg, vs_kstat *simple_cg,

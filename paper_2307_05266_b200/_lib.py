@@ -53,7 +53,7 @@ class VsKstat(C.Structure):
         ("kernel", C.c_int32),
         ("reserved", C.c_int32),
         ("tier", C.c_int32),
-        ("_pad", C.c_int32),
+        ("escape_ppm", C.c_int32),
     ]
 
 

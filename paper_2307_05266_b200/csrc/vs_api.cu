@@ -94,6 +94,12 @@ struct Slab {
     uint2 *meta[4] = {nullptr, nullptr, nullptr, nullptr};
     uint64_t *vrec = nullptr, *prec = nullptr;
     uint32_t *nbr[2] = {nullptr, nullptr};  // TIER-3 neighbour ranks (A, S_hat), built on first use
+    // k_pcgm descriptors (A, S_hat), built on first use
+    uint64_t *desc[2] = {nullptr, nullptr};
+    uint16_t *cidx[2] = {nullptr, nullptr};
+    uint32_t *segtab[2] = {nullptr, nullptr};  // [nseg + 1] first rank | [nseg] x+ base | [nseg] x- base
+    int nseg[2] = {0, 0};
+    int64_t n_escape[2] = {0, 0};
     double *u[NU] = {}, *p[NP] = {};
     Geo geo{};
 };
@@ -116,6 +122,7 @@ struct vs_ctx {
     uint2 *pmeta = nullptr;
     uint64_t *vrec = nullptr, *prec = nullptr;
     double2 *sdiag2 = nullptr;
+    double2 *ctab[2] = {nullptr, nullptr};  // k_pcgm: {1/diag, diag} by code index
     double *invS = nullptr, *d_diag_code = nullptr, *d_invA_enc = nullptr;
     std::vector<int64_t> pstart[4];  // global rank of the first DOF of plane x, x in [0, n]
     std::vector<Slab> slabs;
@@ -433,6 +440,47 @@ Status cg_status_to_error(const CgOut &o, int which) {
     return {VS_OK, ""};
 }
 
+inline bool is_m_alg(int alg) { return alg == CG_TWO_SUM_MQ || alg == CG_TWO_SUM_MRC; }
+
+// k_pcgm descriptors of one slab and operator (vs_cgm.cu): scan the segment
+// starts and x-bases, fill the empty segments on the host, pack.  Runs once,
+// on the first solve that needs it (synchronises the stream).
+void build_descriptors(vs_ctx *c, Slab &S, const CgGroup &G, int op) {
+    const int nseg = (op == 0 ? c->dim : 1) * S.nx;
+    const int64_t m = std::max<int64_t>(1, S.m_own[op]);
+    uint32_t *tab = c->alloc<uint32_t>(3 * (size_t)nseg + 1);
+    int *xp = reinterpret_cast<int *>(tab + nseg + 1), *xm = xp + nseg;
+    CK(cudaMemsetAsync(tab, 0xFF, (size_t)(nseg + 1) * 4, c->stream));
+    CK(cudaMemsetAsync(xp, 0x7F, (size_t)2 * nseg * 4, c->stream));  // 0x7F7F7F7F: "no such neighbour here"
+    launch_desc_scan(c->dim, op, G, c->n, c->nw, tab, xp, xm, c->stream);
+    CK(cudaGetLastError());
+    std::vector<uint32_t> first(nseg + 1);
+    CK(cudaMemcpyAsync(first.data(), tab, (size_t)(nseg + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    first[nseg] = (uint32_t)S.m_own[op];
+    for (int k = nseg - 1; k >= 0; --k)
+        if (first[k] == 0xFFFFFFFFu) first[k] = first[k + 1];  // empty segment
+    CK(cudaMemcpyAsync(tab, first.data(), (size_t)(nseg + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+    S.desc[op] = c->alloc<uint64_t>(m);
+    S.cidx[op] = c->alloc<uint16_t>(m);
+    unsigned long long *cnt = c->alloc<unsigned long long>(1);
+    CK(cudaMemsetAsync(cnt, 0, sizeof *cnt, c->stream));
+    launch_desc_pack(c->dim, op, G, c->n, c->nw, xp, xm, S.desc[op], S.cidx[op], cnt, c->stream);
+    CK(cudaGetLastError());
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();  // `first` must outlive the upload
+    S.n_escape[op] = (int64_t)h;
+    S.segtab[op] = tab;
+    S.nseg[op] = nseg;
+    if (!c->ctab[op]) {
+        const int count = op == 0 ? 16 : 46656;
+        c->ctab[op] = c->alloc<double2>(count);
+        launch_build_ctab(op, c->sdiag2, c->d_diag_code, c->ctab[op], count, c->stream);
+        CK(cudaGetLastError());
+    }
+}
+
 constexpr int GROUP_RING = 8;  // group-table staging slots (>= launches between syncs)
 
 // Launch one fused device PCG solve over all slabs (one cooperative launch)
@@ -487,6 +535,15 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
                 CK(cudaGetLastError());
             }
             G.nbr = nb;
+        }
+        if (is_m_alg((op == 0 ? c->plan_A : c->plan_S).alg)) {
+            if (!S.desc[op]) build_descriptors(c, S, G, op);
+            G.desc = S.desc[op];
+            G.cidx = S.cidx[op];
+            G.nseg = S.nseg[op];
+            G.segstart = S.segtab[op];
+            G.xp = reinterpret_cast<const int *>(S.segtab[op] + S.nseg[op] + 1);
+            G.xm = G.xp + S.nseg[op];
         }
         // k_cg1 buffers (the same slots, paired)
         G.zb[0] = G.z;
@@ -544,6 +601,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     memcpy(P.invA_enc, c->invA_enc, sizeof P.invA_enc);
     P.invS = c->invS;
     P.sdiag2 = c->sdiag2;
+    P.ctab = c->ctab[op];
     // prefetch only where the operator's vectors leave L2 (C1 64^3, L2-resident,
     // on a 46-SM share: A 7.6 -> 8.2 us/it with it); the env value applies as given
     P.pf_dist = (c->pf_forced || m > (int64_t(1) << 20)) ? c->pf_dist : 0;
@@ -561,6 +619,8 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         P.total_blocks = tp.grid;
         P.block_base = 0;
         CK(launch_cg1t(op, tp, P, c->stream));
+    } else if (is_m_alg(pl.alg)) {
+        CK(launch_pcgm(c->dim, op, pl, nloc, P, c->stream));
     } else {
         CK(launch_pcg(c->dim, op, pl, nloc, P, c->stream));
     }
@@ -588,6 +648,11 @@ void drain_log(vs_ctx *c, int from, int64_t *its_op) {
         st.kernel = c->use_tile[op] ? 2 : (op == 0 ? c->plan_A.alg : c->plan_S.alg);
         st.reserved = op == 0 ? c->plan_A.unroll : c->plan_S.unroll;  // P1 DOFs per step
         st.tier = op == 0 ? c->plan_A.tier : c->plan_S.tier;
+        {
+            int64_t esc = 0;
+            for (int q = c->s0; q < c->s1; ++q) esc += c->slabs[q].n_escape[op];
+            st.escape_ppm = m ? (int32_t)(1000000.0 * (double)esc / (double)m) : 0;
+        }
         if (its_op) its_op[li - from] = o.iterations;
         if (m) {
             Status s = cg_status_to_error(o, op);
@@ -863,6 +928,8 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     // 1/2/4 slab groups: A 96.8/99.1/99.6, S_hat 53.5/53.4/54.4).
     // VOXSCHUR_CG=2 forces the reference-order q = A d, =3 the recurrence.
     auto pick = [&](int64_t m, int op) {
+        if (force == 4) return (int)CG_TWO_SUM_MQ;
+        if (force == 5) return (int)CG_TWO_SUM_MRC;
         if (force == 3) return (int)CG_TWO_SUM_QREC;
         if (force == 2) return (int)CG_TWO_SUM;
         if (R == 1 && (force == 1 || (force == 0 && m <= (int64_t)4 * nsm * CG_THREADS)))
@@ -880,8 +947,13 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     // VOXSCHUR_NBR=0 turns it off.  (Ignored by k_cg1.)
     const int nbr_A = en ? nbr : 4;
     const int nbr_S = nbr_A;
-    C->plan_A = pcg_plan(dim, 0, mu_max, nloc, C->device, pick(mu_max, 0), nbr_A, nsm);
-    C->plan_S = pcg_plan(dim, 1, mp_max, nloc, C->device, pick(mp_max, 1), nbr_S, nsm);
+    auto plan = [&](int op, int64_t m, int nbr_tier) {
+        const int alg = pick(m, op);
+        if (is_m_alg(alg)) return pcgm_plan(dim, op, m, nloc, C->device, alg, (op == 0 ? dim : 1) * (C->n + 2), nsm);
+        return pcg_plan(dim, op, m, nloc, C->device, alg, nbr_tier, nsm);
+    };
+    C->plan_A = plan(0, mu_max, nbr_A);
+    C->plan_S = plan(1, mp_max, nbr_S);
     C->sms = nsm;
 }
 

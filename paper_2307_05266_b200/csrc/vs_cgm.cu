@@ -1,0 +1,554 @@
+// vs_cgm.cu -- k_pcgm: the two-reduction inner PCG (krylov.py:76-182) in
+// M-scaled form over 8-byte DOF descriptors -- the HBM-regime kernel.
+//
+// Why.  At 512^3 the two-reduction loop of vs_cg.cu (k_pcg<QR>, packed
+// deltas) already streams at ~5.9 TB/s of DRAM (ncu, profiles/r02a_c4_full.txt)
+// but moves 124 B per DOF per iteration against the 64-B algorithmic figure:
+// x, r, z, d, q are all read and written, the 8-B record is read in both
+// passes and the 12-B neighbour deltas in P1.  This kernel cuts the bytes:
+//
+//  * no r vector.  z = M r is the only residual stored: z -= alpha (M q)
+//    (the recurrence k_cg1 already uses), r_i = diag_i z_i where a sum needs
+//    it (r.z = sum diag z^2).  Rounding differs from r -= alpha q; z = M r in
+//    the last bits; counts and solutions stay inside the parity bar.
+//  * one 8-B descriptor per DOF replaces record + deltas (20 B): 18 bits of
+//    integer codes (S_hat: the six 3-bit face codes; A: no-slip code,
+//    neighbour presence, component), the x+- neighbour ranks as 13-bit
+//    residuals against a per-(component, plane) base held in shared memory,
+//    the y+- ranks as 10-bit distances, z+- = i +- 1.  A DOF whose deltas do
+//    not fit, or whose z/y neighbour wraps, carries an escape mark and takes
+//    the record + bitmask lookup of vs_cg_common.cuh (about 1 % at 512^3).
+//  * two forms of the operator product:
+//    RC = false ("qrec"): s = M q by recurrence, s = M A(z - mu) + beta s_old:
+//         P1 reads z, d_old, s_old, descriptor and gathers 6 neighbour z;
+//         P2 is a pure stream (d, s, x, z and a 2-B code index)  -> 98 B;
+//    RC = true  ("rc"):  q = A d recomputed in both passes from the stored d
+//         (bitwise the same value twice), nothing but x, z, d stored:
+//         P1 reads z, d_old, descriptor (+ 12 gathers), writes d;
+//         P2 reads d, x, z, descriptor (+ 6 gathers), writes x, z   -> 80 B.
+//    Gathers are L1/L2 hits (a neighbour is at most one x-plane away, and the
+//    grid sweeps the vectors front to back), so DRAM sees each value once.
+//
+// Everything else -- the persistent cooperative launch, the deterministic
+// grid sums, the barrier, slab groups and ghost planes -- is vs_cg.cu's.
+#include "vs_cg_common.cuh"
+
+namespace vs {
+
+constexpr int DX_BITS = 13, DY_BITS = 10;
+constexpr uint32_t DX_MASK = (1u << DX_BITS) - 1u, DY_MASK = (1u << DY_BITS) - 1u;
+constexpr uint32_t DX_ESC = DX_MASK;  // x+ field all ones: take the record + bitmask lookup
+constexpr int SH_XP = 18, SH_XM = SH_XP + DX_BITS, SH_YP = SH_XM + DX_BITS, SH_YM = SH_YP + DY_BITS;
+static_assert(SH_YM + DY_BITS == 64, "descriptor is 64 bits");
+
+// the descriptor's 18 code bits as a record the shared helpers understand
+// (coordinates zero: only the escape path needs them, and it reads G.rec)
+template <int OP>
+__device__ __forceinline__ uint64_t desc_rec(uint64_t d) {
+    const uint64_t c = d & 0x3FFFFull;
+    if (OP == 1) return c << 40;
+    return ((c & 0xF) << 36) | (((c >> 4) & 0x3F) << 40) | (((c >> 10) & 0x3) << 33);
+}
+template <int OP>
+__device__ __forceinline__ uint64_t rec_codes(uint64_t rc) {
+    if (OP == 1) return (rc >> 40) & 0x3FFFFull;
+    return (uint64_t)rec_vcode(rc) | (((rc >> 40) & 0x3F) << 4) | ((uint64_t)rec_comp(rc) << 10);
+}
+// 2-B code index of P2's stream: A: no-slip code | component << 8;
+// S_hat: the six face codes in base 6 (46656 values)
+template <int DIM, int OP>
+__device__ __forceinline__ uint32_t rec_cidx(uint64_t rc) {
+    if (OP == 0) return (uint32_t)rec_vcode(rc) | ((uint32_t)rec_comp(rc) << 8);
+    uint32_t v = 0;
+#pragma unroll
+    for (int a = 2; a >= 0; --a) v = v * 6 + (uint32_t)rec_pout(rc, a);
+#pragma unroll
+    for (int a = 2; a >= 0; --a) v = v * 6 + (uint32_t)rec_pin(rc, a);
+    return v;
+}
+template <int DIM, int OP>
+__device__ __forceinline__ int rec_seg(uint64_t rc, int nx) {
+    return (OP == 0 ? rec_comp(rc) * nx : 0) + rec_x(rc);
+}
+
+// ---- descriptor build (once per context and operator) --------------------
+// pass 1: first rank of every (component, plane) segment and the smallest
+// x+ / x- rank distance inside it (the bases the residuals are taken from)
+template <int DIM, int OP>
+__global__ void k_desc_scan(const CgGroup G, int n, int nw, uint32_t *first, int *xp, int *xm) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = i < G.m_own;
+    int seg = -1, dp = INT_MAX, dm = INT_MAX;
+    if (live) {
+        const uint64_t rc = G.rec[i];
+        uint32_t nr[2 * DIM];
+        neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), nw, n, G.nx, rc, i, nr);
+        seg = rec_seg<DIM, OP>(rc, G.nx);
+        if (nr[0] != ABSENT) dp = (int)(nr[0] - i);
+        if (nr[1] != ABSENT) dm = (int)(nr[1] - i);
+    }
+    // a warp's DOFs are consecutive ranks: almost always one segment
+    const int seg0 = __shfl_sync(~0u, seg, 0);
+    if (__all_sync(~0u, seg == seg0) && seg0 >= 0) {
+        const uint32_t fi = __reduce_min_sync(~0u, i);
+        const int mp = __reduce_min_sync(~0u, dp), mm = __reduce_min_sync(~0u, dm);
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(first + seg0, fi);
+            if (mp != INT_MAX) atomicMin(xp + seg0, mp);
+            if (mm != INT_MAX) atomicMin(xm + seg0, mm);
+        }
+    } else if (live) {
+        atomicMin(first + seg, i);
+        if (dp != INT_MAX) atomicMin(xp + seg, dp);
+        if (dm != INT_MAX) atomicMin(xm + seg, dm);
+    }
+}
+// pass 2: pack
+template <int DIM, int OP>
+__global__ void k_desc_pack(const CgGroup G, int n, int nw, const int *xp, const int *xm, uint64_t *desc,
+                            uint16_t *cidx, unsigned long long *n_escape) {
+    constexpr int NS = 2 * DIM;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= G.m_own) return;
+    const uint64_t rc = G.rec[i];
+    uint32_t nr[NS];
+    neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), nw, n, G.nx, rc, i, nr);
+    const int seg = rec_seg<DIM, OP>(rc, G.nx);
+    bool esc = false;
+    uint64_t ex0 = 0, ex1 = 0, dy0 = 0, dy1 = 0;
+    if (nr[0] != ABSENT) {
+        const int64_t e = (int64_t)(int)(nr[0] - i) - xp[seg];
+        if (e < 0 || e >= (int64_t)DX_ESC) esc = true; else ex0 = (uint64_t)e;
+    }
+    if (nr[1] != ABSENT) {
+        const int64_t e = (int64_t)(int)(nr[1] - i) - xm[seg];
+        if (e < 0 || e > (int64_t)DX_MASK) esc = true; else ex1 = (uint64_t)e;
+    }
+    if (DIM == 3) {
+        if (nr[2] != ABSENT) {
+            const int64_t e = (int64_t)nr[2] - (int64_t)i;
+            if (e < 1 || e > (int64_t)DY_MASK) esc = true; else dy0 = (uint64_t)e;
+        }
+        if (nr[3] != ABSENT) {
+            const int64_t e = (int64_t)i - (int64_t)nr[3];
+            if (e < 1 || e > (int64_t)DY_MASK) esc = true; else dy1 = (uint64_t)e;
+        }
+    }
+    if (nr[NS - 2] != ABSENT && nr[NS - 2] != i + 1) esc = true;
+    if (nr[NS - 1] != ABSENT && nr[NS - 1] != i - 1) esc = true;
+    if (esc) {
+        ex0 = DX_ESC;
+        atomicAdd(n_escape, 1ull);
+    }
+    desc[i] = rec_codes<OP>(rc) | (ex0 << SH_XP) | (ex1 << SH_XM) | (dy0 << SH_YP) | (dy1 << SH_YM);
+    cidx[i] = (uint16_t)rec_cidx<DIM, OP>(rc);
+}
+// {1/diag, diag} by code index
+__global__ void k_build_ctab(int op, const double2 *sdiag2, const double *diag_code, double2 *ctab, int count) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    if (op == 0) {
+        const double d = diag_code[k & 15];
+        ctab[k] = make_double2(d != 0.0 ? 1.0 / d : 0.0, d);  // krylov.py:213
+        return;
+    }
+    uint32_t v = (uint32_t)k, key = 0;
+    for (int f = 0; f < 6; ++f) {
+        key |= (v % 6u) << (3 * f);
+        v /= 6u;
+    }
+    ctab[k] = sdiag2[key];
+}
+
+void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *first, int *xp, int *xm,
+                      cudaStream_t s) {
+    if (!G.m_own) return;
+    const unsigned nb = (G.m_own + 255) / 256;
+    if (dim == 3)
+        op == 0 ? k_desc_scan<3, 0><<<nb, 256, 0, s>>>(G, n, nw, first, xp, xm)
+                : k_desc_scan<3, 1><<<nb, 256, 0, s>>>(G, n, nw, first, xp, xm);
+    else
+        op == 0 ? k_desc_scan<2, 0><<<nb, 256, 0, s>>>(G, n, nw, first, xp, xm)
+                : k_desc_scan<2, 1><<<nb, 256, 0, s>>>(G, n, nw, first, xp, xm);
+}
+void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int *xp, const int *xm, uint64_t *desc,
+                      uint16_t *cidx, unsigned long long *n_escape, cudaStream_t s) {
+    if (!G.m_own) return;
+    const unsigned nb = (G.m_own + 255) / 256;
+    if (dim == 3)
+        op == 0 ? k_desc_pack<3, 0><<<nb, 256, 0, s>>>(G, n, nw, xp, xm, desc, cidx, n_escape)
+                : k_desc_pack<3, 1><<<nb, 256, 0, s>>>(G, n, nw, xp, xm, desc, cidx, n_escape);
+    else
+        op == 0 ? k_desc_pack<2, 0><<<nb, 256, 0, s>>>(G, n, nw, xp, xm, desc, cidx, n_escape)
+                : k_desc_pack<2, 1><<<nb, 256, 0, s>>>(G, n, nw, xp, xm, desc, cidx, n_escape);
+}
+void launch_build_ctab(int op, const double2 *sdiag2, const double *diag_code, double2 *ctab, int count,
+                       cudaStream_t s) {
+    k_build_ctab<<<(count + 255) / 256, 256, 0, s>>>(op, sdiag2, diag_code, ctab, count);
+}
+
+// ---- the kernel -----------------------------------------------------------
+template <int DIM, int OP, bool RC, int NT>
+__global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
+    constexpr bool PROJ = (OP == 1);
+    constexpr int NS = 2 * DIM;
+    extern __shared__ __align__(16) uint8_t dyn_smem[];  // segment tables
+    __shared__ double s_tab[40];
+    __shared__ double s_warp[NT / 32][5];
+    __shared__ double s_tot[5];
+    __shared__ __align__(16) double s_val[4][NT];  // grid_sum staging
+    __shared__ CgGroup G;
+    const int grp = P.group_base + blockIdx.x / P.bpg;
+    if (threadIdx.x == 0) G = P.groups[grp];
+    if (threadIdx.x < 16) {
+        s_tab[threadIdx.x] = P.diag_code[threadIdx.x];
+        s_tab[16 + threadIdx.x] = P.inv_code[threadIdx.x];
+        if (threadIdx.x < 8) s_tab[32 + threadIdx.x] = P.invA_enc[threadIdx.x];
+    }
+    unsigned gen = __ldcg(P.bar_base);
+    __syncthreads();
+    const int nseg = G.nseg;
+    uint32_t *s_seg = reinterpret_cast<uint32_t *>(dyn_smem);  // [nseg + 1] first rank of each segment
+    int *s_xp = reinterpret_cast<int *>(s_seg + nseg + 1);      // [nseg] x+ base
+    int *s_xm = s_xp + nseg;                                    // [nseg] x- base
+    for (int k = threadIdx.x; k <= nseg; k += NT) s_seg[k] = G.segstart[k];
+    for (int k = threadIdx.x; k < nseg; k += NT) {
+        s_xp[k] = G.xp[k];
+        s_xm[k] = G.xm[k];
+    }
+    __syncthreads();
+    const Tabs T{s_tab, s_tab + 16, s_tab + 32, P.invS};
+    const double2 *sdg = P.sdiag2;
+    const double2 *ctab = P.ctab;
+    __builtin_assume(__isGlobal(ctab));
+    const uint32_t m = G.m_own, m_all = G.m_all;
+    const uint32_t tid = (blockIdx.x % P.bpg) * NT + threadIdx.x;
+    const uint32_t stride = P.bpg * NT;
+    double *x = G.x, *z = G.z, *sv = G.q;
+    const uint64_t *desc = G.desc;
+    const uint16_t *cidx = G.cidx;
+    const uint64_t *rec = G.rec;
+    const bool halo = G.zpeer[0] != nullptr;
+    __builtin_assume(__isGlobal(x));
+    __builtin_assume(__isGlobal(z));
+    __builtin_assume(__isGlobal(sv));
+    __builtin_assume(__isGlobal(desc));
+    __builtin_assume(__isGlobal(cidx));
+    __builtin_assume(__isGlobal(rec));
+    const double inv_h = P.inv_h, inv_h2 = P.inv_h2;
+
+    // descriptor -> record bits and neighbour ranks
+    auto decode = [&](uint64_t d, uint32_t i, int seg, uint64_t &rc, uint32_t (&nr)[NS]) {
+        const uint32_t fx = (uint32_t)(d >> SH_XP) & DX_MASK;
+        if (fx == DX_ESC) {
+            rc = rec[i];
+            neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, i, nr);
+            return;
+        }
+        rc = desc_rec<OP>(d);
+        nr[0] = rec_has_nb<OP>(rc, 0) ? i + (uint32_t)(s_xp[seg] + (int)fx) : ABSENT;
+        nr[1] = rec_has_nb<OP>(rc, 1) ? i + (uint32_t)(s_xm[seg] + (int)((uint32_t)(d >> SH_XM) & DX_MASK)) : ABSENT;
+        if (DIM == 3) {
+            nr[2] = rec_has_nb<OP>(rc, 2) ? i + ((uint32_t)(d >> SH_YP) & DY_MASK) : ABSENT;
+            nr[3] = rec_has_nb<OP>(rc, 3) ? i - ((uint32_t)(d >> SH_YM) & DY_MASK) : ABSENT;
+        }
+        nr[NS - 2] = rec_has_nb<OP>(rc, NS - 2) ? i + 1 : ABSENT;
+        nr[NS - 1] = rec_has_nb<OP>(rc, NS - 1) ? i - 1 : ABSENT;
+    };
+
+    // ---- setup (krylov.py:102-119): project rhs; r = op(x0) - rhs; z = M^-1 r
+    double mu_rhs = 0.0, mu = 0.0, rz = 0.0, rp0 = 0.0, ru0 = 0.0;
+    if (PROJ) {
+        double v[1] = {0.0};
+        for (uint32_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], G.rhs[i]);
+        grid_sum<1, false, NT>(v, 0, P, gen, s_val, s_tot);
+        mu_rhs = v[0] / P.m_global;
+    }
+    {
+        double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        const double *x0 = G.x0;
+        for (uint32_t i = tid; i < m; i += stride) {
+            const uint64_t rc = rec[i];
+            double ax = 0.0, xi = 0.0;
+            if (x0) {
+                uint32_t nr[NS];
+                neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, i, nr);
+                xi = x0[i];
+                double vn[NS];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) vn[s] = nr[s] != ABSENT ? x0[nr[s]] : 0.0;
+                ax = op_value<DIM, OP>(rc, xi, vn, T, inv_h, inv_h2);
+                if (x0 != x) x[i] = xi;
+            } else {
+                x[i] = 0.0;
+            }
+            const double b = PROJ ? __dsub_rn(G.rhs[i], mu_rhs) : G.rhs[i];
+            const double ri = __dsub_rn(ax, b);
+            const double zi = __dmul_rn(ri, jacobi_inv<OP>(rc, T));
+            z[i] = zi;
+            if (halo) halo_store(G, OP == 0 ? rec_comp(rc) : 0, i, zi);
+            v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
+            v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
+            v[2] = __dadd_rn(v[2], __dmul_rn(ri, ri));
+            v[3] = __dadd_rn(v[3], zi);
+            v[4] = __dadd_rn(v[4], ri);
+        }
+        grid_sum_shfl<5, true, NT>(v, 1, P, gen, s_warp, s_tot);
+        if (PROJ) {
+            mu = v[3] / P.m_global;
+            v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
+            v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
+        }
+        rz = v[0];
+        rp0 = sqrt(v[1]);
+        ru0 = sqrt(v[2]);
+    }
+    const double ref = rp0;  // inner solves stop on the preconditioned norm (schur.py:207-210, :259-262)
+    double beta = 0.0, rp_last = rp0, sval = 0.0;
+    int status = 0;
+    int64_t sat = 0, its = 0;
+    bool conv = (ref == 0.0);
+    double *dold = G.d0, *dnew = G.d1;
+    __builtin_assume(__isGlobal(dold));
+    __builtin_assume(__isGlobal(dnew));
+    unsigned long long ph[4] = {0, 0, 0, 0};
+    if (!conv) {
+        for (int64_t it = 0; it < P.max_iter; ++it) {
+            if (rz < 0.0) { status = 1; sval = rz; sat = it; break; }
+            if (rz == 0.0) { conv = true; break; }
+            const bool first = it == 0;
+            const uint64_t t0 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
+            // ---- P1: d = (z - mu) + beta d_old; d.q
+            double v1[1] = {0.0};
+            {
+                uint64_t dn_ = tid < m ? __ldcs(desc + tid) : 0;  // the next DOF's descriptor, carried across the step
+                int seg = 0;
+                for (uint32_t i = tid; i < m; i += stride) {
+                    const uint32_t ip = i + P.pf_dist * stride;
+                    if (P.pf_dist && ip < m) {  // the own streams pf_dist strides ahead (L2, no registers)
+                        prefetch_l2(z + ip);
+                        prefetch_l2(desc + ip);
+                        if (!first) {
+                            prefetch_l2(dold + ip);
+                            if (!RC) prefetch_l2(sv + ip);
+                        }
+                    }
+                    const uint64_t d = dn_;
+                    while (seg + 1 < nseg && i >= s_seg[seg + 1]) ++seg;
+                    const double zc = z[i];
+                    const double dc = first ? 0.0 : dold[i];
+                    const double so = (RC || first) ? 0.0 : sv[i];
+                    uint64_t rc;
+                    uint32_t nr[NS];
+                    decode(d, i, seg, rc, nr);
+                    double zn[NS], dn[NS];
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) {  // unconditional loads (absent -> own index)
+                        const uint32_t j = nr[s] != ABSENT ? nr[s] : i;
+                        zn[s] = z[j];
+                        dn[s] = (RC && !first) ? dold[j] : 0.0;
+                    }
+                    if (i + stride < m) dn_ = __ldcs(desc + i + stride);
+                    const double zp = PROJ ? __dsub_rn(zc, mu) : zc;
+                    const double di = first ? zp : __dadd_rn(zp, __dmul_rn(beta, dc));
+                    double vn[NS];
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) {
+                        double zj = PROJ ? __dsub_rn(zn[s], mu) : zn[s];
+                        if (RC && !first) zj = __dadd_rn(zj, __dmul_rn(beta, dn[s]));
+                        // A needs 0.0 at absent slots (left fold); S_hat's absent faces
+                        // carry weight 0.0 (op_value), so the clamped value is harmless
+                        vn[s] = (OP == 0 && nr[s] == ABSENT) ? 0.0 : zj;
+                    }
+                    dnew[i] = di;
+                    if (RC) {
+                        const double qi = op_value<DIM, OP>(rc, di, vn, T, inv_h, inv_h2);
+                        v1[0] = __dadd_rn(v1[0], __dmul_rn(di, qi));
+                    } else {
+                        double inv, dg;
+                        inv_diag<OP>(rc, T, sdg, inv, dg);
+                        const double mw = __dmul_rn(op_value<DIM, OP>(rc, zp, vn, T, inv_h, inv_h2), inv);
+                        const double si = first ? mw : __dadd_rn(mw, __dmul_rn(beta, so));
+                        sv[i] = si;
+                        v1[0] = __dadd_rn(v1[0], __dmul_rn(di, __dmul_rn(dg, si)));
+                    }
+                }
+                // ghost-plane d, recomputed exactly as the owning slab computes it
+                if (RC)
+                    for (uint32_t i = m + tid; i < m_all; i += stride) {
+                        double zc = z[i];
+                        if (PROJ) zc = __dsub_rn(zc, mu);
+                        dnew[i] = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dold[i]));
+                    }
+            }
+            const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
+            grid_sum<1, false, NT>(v1, 2, P, gen, s_val, s_tot);
+            const uint64_t t2 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
+            const double dq = v1[0];
+            if (dq <= 0.0) { status = 2; sval = dq; sat = it; break; }
+            const double alpha = rz / dq;
+            // ---- P2: x -= alpha d; z -= alpha M q; sums r.z = sum diag z^2, z.z
+            // (+ sum z, sum r when projected)
+            constexpr int KL = PROJ ? 4 : 2;
+            double v[KL];
+#pragma unroll
+            for (int s = 0; s < KL; ++s) v[s] = 0.0;
+            if (RC) {
+                uint64_t dn_ = tid < m ? __ldcs(desc + tid) : 0;
+                int seg = 0;
+                for (uint32_t i = tid; i < m; i += stride) {
+                    const uint32_t ip = i + P.pf_dist * stride;
+                    if (P.pf_dist && ip < m) {
+                        prefetch_l2(dnew + ip);
+                        prefetch_l2(x + ip);
+                        prefetch_l2(z + ip);
+                        prefetch_l2(desc + ip);
+                    }
+                    const uint64_t d = dn_;
+                    while (seg + 1 < nseg && i >= s_seg[seg + 1]) ++seg;
+                    const double di = dnew[i], xo = x[i], zo = z[i];
+                    uint64_t rc;
+                    uint32_t nr[NS];
+                    decode(d, i, seg, rc, nr);
+                    double vn[NS];
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) {
+                        const double dj = dnew[nr[s] != ABSENT ? nr[s] : i];
+                        vn[s] = (OP == 0 && nr[s] == ABSENT) ? 0.0 : dj;
+                    }
+                    if (i + stride < m) dn_ = __ldcs(desc + i + stride);
+                    double inv, dg;
+                    inv_diag<OP>(rc, T, sdg, inv, dg);
+                    const double qi = op_value<DIM, OP>(rc, di, vn, T, inv_h, inv_h2);
+                    const double xi = __dsub_rn(xo, __dmul_rn(alpha, di));
+                    const double zi = __dsub_rn(zo, __dmul_rn(alpha, __dmul_rn(qi, inv)));
+                    x[i] = xi;
+                    z[i] = zi;
+                    if (halo) halo_store(G, OP == 0 ? rec_comp(rc) : 0, i, zi);
+                    const double ri = __dmul_rn(dg, zi);
+                    v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
+                    v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
+                    if (PROJ) {
+                        v[2] = __dadd_rn(v[2], zi);
+                        v[3] = __dadd_rn(v[3], ri);
+                    }
+                }
+            } else {
+                for (uint32_t i = tid; i < m; i += stride) {
+                    const uint32_t ip = i + P.pf_dist * stride;
+                    if (P.pf_dist && ip < m) {
+                        prefetch_l2(dnew + ip);
+                        prefetch_l2(sv + ip);
+                        prefetch_l2(x + ip);
+                        prefetch_l2(z + ip);
+                    }
+                    const double di = dnew[i], si = sv[i], xo = x[i], zo = z[i];
+                    const uint32_t ci = __ldcs(cidx + i);
+                    const double2 t = __ldg(ctab + (OP == 0 ? (ci & 0xFFu) : ci));
+                    const double xi = __dsub_rn(xo, __dmul_rn(alpha, di));
+                    const double zi = __dsub_rn(zo, __dmul_rn(alpha, si));
+                    x[i] = xi;
+                    z[i] = zi;
+                    if (halo) halo_store(G, OP == 0 ? (int)(ci >> 8) : 0, i, zi);
+                    const double ri = __dmul_rn(t.y, zi);
+                    v[0] = __dadd_rn(v[0], __dmul_rn(ri, zi));
+                    v[1] = __dadd_rn(v[1], __dmul_rn(zi, zi));
+                    if (PROJ) {
+                        v[2] = __dadd_rn(v[2], zi);
+                        v[3] = __dadd_rn(v[3], ri);
+                    }
+                }
+            }
+            const uint64_t t3 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
+            grid_sum<KL, true, NT>(v, 3, P, gen, s_val, s_tot);
+            if (P.phase_ns && threadIdx.x == 0) {
+                const uint64_t t4 = gtimer();
+                ph[0] += t1 - t0;
+                ph[1] += t2 - t1;
+                ph[2] += t3 - t2;
+                ph[3] += t4 - t3;
+            }
+            if (PROJ) {
+                mu = v[2] / P.m_global;
+                v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[3]));
+                v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[2]));
+            }
+            const double rz_new = v[0];
+            beta = rz_new / rz;
+            rz = rz_new;
+            const double nz = sqrt(v[1]);
+            if (!isfinite(nz)) { status = 3; sat = it + 1; break; }
+            its = it + 1;
+            rp_last = nz;
+            double *t = dold; dold = dnew; dnew = t;
+            if (nz / ref < P.tol) { conv = true; break; }
+        }
+    }
+    if (P.phase_ns && threadIdx.x == 0) {  // [0..3] block 0, [4..7] max, [8..11] sum over blocks
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            if (blockIdx.x == 0) P.phase_ns[p] += ph[p];
+            atomicMax(P.phase_ns + 4 + p, ph[p]);
+            atomicAdd(P.phase_ns + 8 + p, ph[p]);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *P.bar_base = gen;  // the next launch on this stream starts from here
+        CgOut *o = P.out;
+        o->iterations = its;
+        o->converged = conv ? 1 : 0;
+        o->status = status;
+        o->value = sval;
+        o->at_iter = sat;
+        o->res_prec0 = rp0;
+        o->res_unprec0 = ru0;
+        o->res_prec_last = rp_last;
+        o->res_unprec_last = ru0;
+    }
+}
+
+template <int DIM, int OP>
+static const void *pcgm_fn_t(bool rc, int nt) {
+    if (nt == 512) return rc ? (const void *)k_pcgm<DIM, OP, true, 512> : (const void *)k_pcgm<DIM, OP, false, 512>;
+    return rc ? (const void *)k_pcgm<DIM, OP, true, CG_THREADS> : (const void *)k_pcgm<DIM, OP, false, CG_THREADS>;
+}
+static const void *pcgm_fn(int dim, int op, bool rc, int nt) {
+    if (dim == 3) return op == 0 ? pcgm_fn_t<3, 0>(rc, nt) : pcgm_fn_t<3, 1>(rc, nt);
+    return op == 0 ? pcgm_fn_t<2, 0>(rc, nt) : pcgm_fn_t<2, 1>(rc, nt);
+}
+
+// Plan: one block per SM (per group), segment tables in dynamic smem.
+CgPlan pcgm_plan(int dim, int op, int64_t m, int groups, int device, int alg, int nseg_max, int sms) {
+    CgPlan pl{};
+    pl.alg = alg;
+    pl.unroll = 1;
+    pl.tier = 5;
+    int nt = CG_THREADS;
+    if (const char *e = getenv("VOXSCHUR_M_THREADS"))
+        if (atoi(e) == 512 || atoi(e) == CG_THREADS) nt = atoi(e);
+    pl.threads = nt;
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    if (sms > 0 && sms < nsm) nsm = sms;
+    const void *fn = pcgm_fn(dim, op, alg == CG_TWO_SUM_MRC, nt);
+    pl.smem = (size_t)(3 * nseg_max + 1) * 4;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, pl.smem);
+    if (per_sm < 1) per_sm = 1;
+    if (const char *e = getenv("VOXSCHUR_M_BLOCKS_PER_SM"))
+        if (atoi(e) >= 1 && atoi(e) < per_sm) per_sm = atoi(e);
+    pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * nsm / groups, (m + nt - 1) / nt));
+    pl.slots = 0;
+    return pl;
+}
+
+cudaError_t launch_pcgm(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s) {
+    P.cache_slots = 0;
+    P.bpg = pl.grid;
+    void *args[] = {&P};
+    return cudaLaunchCooperativeKernel(pcgm_fn(dim, op, pl.alg == CG_TWO_SUM_MRC, pl.threads), dim3(pl.grid * groups),
+                                       dim3(pl.threads), args, pl.smem, s);
+}
+
+}  // namespace vs

@@ -35,6 +35,13 @@ struct CgGroup {
     const double *rhs, *x0;
     double *x, *r, *z, *d0, *d1, *q;
     double *zb[2], *ub[2], *sb[2];  // k_cg1: double-buffered zr = M r, u = M A zr, s = M q
+    // k_pcgm (vs_cgm.cu): 8-B descriptors, 2-B code indices and the per-segment
+    // tables (segment = (component, x-plane): first rank, x+ base, x- base)
+    const uint64_t *desc;
+    const uint16_t *cidx;
+    const uint32_t *segstart;
+    const int *xp, *xm;
+    int nseg;
     const uint32_t *nbr;            // TIER 3: neighbour ranks [2*dim][m_own] (ABSENT if none);
                                     // TIER 4: int2 x-deltas [m_own], then short2 y-deltas [m_own] (3D)
     // halo: side s = 0 sends the first owned plane to the lower neighbour's
@@ -68,6 +75,7 @@ struct CgParams {
     double invA_enc[8];
     const double *invS;
     const double2 *sdiag2;         // S_hat {1/diag, diag} by 18-bit key (k_cg1)
+    const double2 *ctab;           // {1/diag, diag} by 2-B code index (k_pcgm)
     uint32_t cache_slots;
     uint32_t pf_dist;              // L2 prefetch distance in grid strides (0 = off)
     unsigned long long *phase_ns;  // optional [12] accumulators
@@ -123,7 +131,9 @@ int64_t cc_label_device(const uint8_t *d_fluid, int dim, int n, int *d_labels, v
 constexpr size_t CG_SMEM_BUDGET = 200 * 1024;  // dynamic smem per block (1 block / SM)
 // k_pcg (reference order) | k_cg1 (one reduction) | k_pcg with q = A z + beta q_old
 // (value 3: 2 is the k_cg1t kernel id in vs_kstat)
-enum CgAlg { CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3 };
+// 4, 5: k_pcgm (vs_cgm.cu), M-scaled over 8-B descriptors: s = M q by
+// recurrence / q = A d recomputed in both passes
+enum CgAlg { CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3, CG_TWO_SUM_MQ = 4, CG_TWO_SUM_MRC = 5 };
 struct CgPlan {
     int alg;
     int unroll;   // DOFs per P1 step (k_pcg<QR> only)
@@ -138,6 +148,15 @@ CgPlan pcg_plan(int dim, int op, int64_t m, int groups, int device, int alg, int
 void launch_build_nbr(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *out, cudaStream_t s,
                       int tier = 3);
 cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
+// k_pcgm (vs_cgm.cu)
+CgPlan pcgm_plan(int dim, int op, int64_t m, int groups, int device, int alg, int nseg_max, int sms = 0);
+cudaError_t launch_pcgm(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
+void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *first, int *xp, int *xm,
+                      cudaStream_t s);
+void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int *xp, const int *xm, uint64_t *desc,
+                      uint16_t *cidx, unsigned long long *n_escape, cudaStream_t s);
+void launch_build_ctab(int op, const double2 *sdiag2, const double *diag_code, double2 *ctab, int count,
+                       cudaStream_t s);
 
 // ---- k_cg1t: plane-sweep tiles staged by TMA (vs_cgt.cu) ----------------
 // A unit = one DOF family (velocity component / pressure), a run of own
