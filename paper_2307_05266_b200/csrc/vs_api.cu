@@ -99,6 +99,7 @@ struct Slab {
     uint16_t *cidx[2] = {nullptr, nullptr};
     uint32_t *segtab[2] = {nullptr, nullptr};  // [nseg + 1] first rank | [nseg] x+ base | [nseg] x- base
     int nseg[2] = {0, 0};
+    int nstrip[2] = {1, 1};  // k_pcgs: strips per segment
     int64_t n_escape[2] = {0, 0};
     double *u[NU] = {}, *p[NP] = {};
     Geo geo{};
@@ -200,7 +201,22 @@ struct vs_ctx {
             if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
     }
-    void sync() { CK(cudaStreamSynchronize(stream)); }
+    // multi-GPU runs: a cross-GPU barrier that gave up sets *xflag_dev (device memory, read back after a sync)
+    int *xflag_dev = nullptr;
+    unsigned long long xtimeout_ns = 0;
+    void sync() {
+        CK(cudaStreamSynchronize(stream));
+        if (xflag_dev) {
+            int h = 0;
+            CK(cudaMemcpy(&h, xflag_dev, sizeof h, cudaMemcpyDeviceToHost));
+            if (h) {
+                char buf[200];
+                snprintf(buf, sizeof buf, "cross-rank barrier timed out after %.0f s: a peer rank never arrived "
+                         "(this context is unusable; destroy it on every rank)", (double)xtimeout_ns * 1e-9);
+                throw Status{VS_ECUDA, buf};
+            }
+        }
+    }
     int nfam() const { return dim; }
     // ---- slab-distributed helpers.  Slabs [s0, s1) are local (all of them
     // in one process, or this rank's one on a multi-process run); remote
@@ -218,7 +234,7 @@ struct vs_ctx {
     // cross-rank device barrier (one arrival per rank; same counter as the CG)
     void xbar() {
         if (!mp()) return;
-        launch_xbar(bar, bar_base, nranks, stream);
+        launch_xbar(bar, bar_base, nranks, xflag_dev, xtimeout_ns, stream);
         ++launches;
     }
     // make this rank's reduction slots [q0, q1) visible in every rank's scal
@@ -428,6 +444,7 @@ Status cg_status_to_error(const CgOut &o, int which) {
         snprintf(buf, sizeof buf, "non-finite residual at iteration %lld", (long long)o.at_iter);
         return {VS_ERUNTIME, buf};
     }
+    if (o.status == 4) return {VS_ECUDA, "cross-rank barrier timed out inside a fused inner solve"};
     if (!o.converged) {
         // schur.py:214-218 / :266-271
         snprintf(buf, sizeof buf,
@@ -440,7 +457,8 @@ Status cg_status_to_error(const CgOut &o, int which) {
     return {VS_OK, ""};
 }
 
-inline bool is_m_alg(int alg) { return alg == CG_TWO_SUM_MQ || alg == CG_TWO_SUM_MRC; }
+inline bool is_sweep_alg(int alg) { return alg == CG_SWEEP_MQ || alg == CG_SWEEP_MRC; }
+inline bool is_m_alg(int alg) { return alg == CG_TWO_SUM_MQ || alg == CG_TWO_SUM_MRC || is_sweep_alg(alg); }
 
 // k_pcgm descriptors of one slab and operator (vs_cgm.cu): scan the segment
 // starts and x-bases, fill the empty segments on the host, pack.  Runs once,
@@ -461,6 +479,9 @@ void build_descriptors(vs_ctx *c, Slab &S, const CgGroup &G, int op) {
     for (int k = nseg - 1; k >= 0; --k)
         if (first[k] == 0xFFFFFFFFu) first[k] = first[k + 1];  // empty segment
     CK(cudaMemcpyAsync(tab, first.data(), (size_t)(nseg + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+    uint32_t lmax = 1;
+    for (int k = 0; k < nseg; ++k) lmax = std::max(lmax, first[k + 1] - first[k]);
+    S.nstrip[op] = (int)((lmax + CG_THREADS - 1) / CG_THREADS);
     S.desc[op] = c->alloc<uint64_t>(m);
     S.cidx[op] = c->alloc<uint16_t>(m);
     unsigned long long *cnt = c->alloc<unsigned long long>(1);
@@ -541,6 +562,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
             G.desc = S.desc[op];
             G.cidx = S.cidx[op];
             G.nseg = S.nseg[op];
+            G.nstrip = S.nstrip[op];
             G.segstart = S.segtab[op];
             G.xp = reinterpret_cast<const int *>(S.segtab[op] + S.nseg[op] + 1);
             G.xm = G.xp + S.nseg[op];
@@ -582,9 +604,12 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.bar_base = c->bar_base;
     P.npart = c->npart;
     P.xgpu = c->mp() ? 1 : 0;
+    P.xflag = c->xflag_dev;
+    P.xtimeout_ns = c->xtimeout_ns;
     P.part_self = c->mp() ? c->rank : 0;
     for (int r = 0; r < c->npart; ++r) P.part_peer[r] = c->part_peer[r];
     P.phase_ns = c->phase_ns;
+    if (const char *e = getenv("VOXSCHUR_DBG")) P.dbg = (uint32_t)atoi(e);
     P.out = c->cglog + li;
     P.tol = eps;
     P.max_iter = std::max<int64_t>(1000, 2 * m);  // schur.py:196-197
@@ -605,6 +630,8 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     // prefetch only where the operator's vectors leave L2 (C1 64^3, L2-resident,
     // on a 46-SM share: A 7.6 -> 8.2 us/it with it); the env value applies as given
     P.pf_dist = (c->pf_forced || m > (int64_t(1) << 20)) ? c->pf_dist : 0;
+    // k_pcgs prefetches whole units: two steps ahead unless VOXSCHUR_PREFETCH says otherwise
+    if (is_sweep_alg((op == 0 ? c->plan_A : c->plan_S).alg)) P.pf_dist = c->pf_forced ? c->pf_dist : 2;
     const CgPlan &pl = op == 0 ? c->plan_A : c->plan_S;
     P.total_blocks = pl.grid * R;          // blocks of every rank
     P.block_base = pl.grid * c->s0;        // global index of this launch's block 0
@@ -619,6 +646,15 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         P.total_blocks = tp.grid;
         P.block_base = 0;
         CK(launch_cg1t(op, tp, P, c->stream));
+    } else if (is_sweep_alg(pl.alg)) {
+        CgPlan ps = pl;  // the unit table of a block's run, sized now that the strips are known
+        int64_t units = 1;
+        for (int q = c->s0; q < c->s1; ++q)
+            units = std::max<int64_t>(units, (int64_t)c->slabs[q].nseg[op] * c->slabs[q].nstrip[op]);
+        ps.smem = (size_t)(units / ps.grid + 2) * 16;
+        if (!pcgs_fits(c->dim, op, ps, c->device))
+            throw Status{VS_ECUDA, "k_pcgs: the unit table does not fit shared memory"};
+        CK(launch_pcgs(c->dim, op, ps, nloc, P, c->stream));
     } else if (is_m_alg(pl.alg)) {
         CK(launch_pcgm(c->dim, op, pl, nloc, P, c->stream));
     } else {
@@ -928,6 +964,8 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     // 1/2/4 slab groups: A 96.8/99.1/99.6, S_hat 53.5/53.4/54.4).
     // VOXSCHUR_CG=2 forces the reference-order q = A d, =3 the recurrence.
     auto pick = [&](int64_t m, int op) {
+        if (force == 6) return (int)CG_SWEEP_MQ;
+        if (force == 7) return (int)CG_SWEEP_MRC;
         if (force == 4) return (int)CG_TWO_SUM_MQ;
         if (force == 5) return (int)CG_TWO_SUM_MRC;
         if (force == 3) return (int)CG_TWO_SUM_QREC;
@@ -949,6 +987,7 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     const int nbr_S = nbr_A;
     auto plan = [&](int op, int64_t m, int nbr_tier) {
         const int alg = pick(m, op);
+        if (is_sweep_alg(alg)) return pcgs_plan(dim, op, m, nloc, C->device, alg, 1, nsm);
         if (is_m_alg(alg)) return pcgm_plan(dim, op, m, nloc, C->device, alg, (op == 0 ? dim : 1) * (C->n + 2), nsm);
         return pcg_plan(dim, op, m, nloc, C->device, alg, nbr_tier, nsm);
     };
@@ -1307,6 +1346,14 @@ static int create_common(const uint8_t *fluid, int dim, int n, int flow_dir, int
         C->sdiag_ok = hflag == 0;
         // ---- decomposition into x-slabs (1 = whole domain), work vectors, plans
         build_slabs(C, slabs, rank, nranks);
+        if (nranks > 1) {
+            // cross-GPU barriers give up after VOXSCHUR_XBAR_TIMEOUT_S seconds (default 60)
+            C->xflag_dev = C->alloc<int>(1);
+            CK(cudaMemsetAsync(C->xflag_dev, 0, sizeof(int), C->stream));
+            const char *et = getenv("VOXSCHUR_XBAR_TIMEOUT_S");
+            const double secs = et && atof(et) > 0 ? atof(et) : 60.0;
+            C->xtimeout_ns = (unsigned long long)(secs * 1e9);
+        }
         if (const char *pf = getenv("VOXSCHUR_PREFETCH")) {
             C->pf_dist = (uint32_t)atoi(pf);
             C->pf_forced = true;

@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
         for (int64_t it = 0; it < P.max_iter; ++it) {
             if (rz < 0.0) { status = 1; sval = rz; sat = it; break; }
             if (rz == 0.0) { conv = true; break; }
+            if (P.xgpu && *P.xflag) { status = 4; sat = it; break; }  // a peer rank never arrived
             const uint64_t t0 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             // ---- P1: d = z - mu + beta d_old, q = op(d), d.q  (instantiated
             // separately for the first iteration, where d = z - mu)
@@ -590,6 +591,7 @@ __global__ void __launch_bounds__(NT, 1) k_cg1(const CgParams P) {
         for (int64_t it = 0; it < P.max_iter; ++it) {
             if (gamma < 0.0) { status = 1; sval = gamma; sat = it; break; }
             if (gamma == 0.0) { conv = true; break; }
+            if (P.xgpu && *P.xflag) { status = 4; sat = it; break; }  // a peer rank never arrived
             double beta, dq;
             if (it == 0) {
                 beta = 0.0;

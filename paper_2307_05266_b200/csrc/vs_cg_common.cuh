@@ -160,8 +160,14 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
 // (the reds form one release sequence); it is 0.13 us cheaper than a
 // fence.acq_rel (B200, 148 x 1024 threads: 1.17 vs 1.30 us per barrier;
 // the unfenced floor is 0.84 us -- tools/gridsync_variants.cu).
+// xflag (multi-GPU runs only): this rank's "a peer never arrived" flag, in
+// device memory.  A cross-GPU barrier that waits longer than
+// xtimeout_ns sets it and gives up; every later barrier of the rank returns
+// at once, the fused loops stop at their next iteration (status 4) and the
+// host raises VS_ECUDA after its next synchronisation instead of hanging.
 __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, unsigned total_blocks,
-                                             bool xgpu = false) {
+                                             bool xgpu = false, volatile int *xflag = nullptr,
+                                             unsigned long long xtimeout_ns = 0) {
     __syncthreads();
     target += total_blocks;
     if (threadIdx.x == 0) {
@@ -172,8 +178,20 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, un
             // GPUs' stores visible here
             asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
             unsigned v;
+            unsigned long long t0 = 0;
+            unsigned spins = 0;
             do {
                 asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+                if (xflag && (++spins & 1023u) == 0) {  // look at the clock every 1024 polls
+                    unsigned long long now;
+                    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+                    if (!t0) t0 = now;
+                    if (*xflag) break;
+                    if (xtimeout_ns && now - t0 > xtimeout_ns) {
+                        *xflag = 1;
+                        break;
+                    }
+                }
             } while ((int)(v - target) < 0);
             asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.sys.global.u32 t, [%0];\n\t}" ::"l"(bar) : "memory");
         } else {
@@ -239,7 +257,7 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
             for (int k = 0; k < K; ++k) dst[k] = t[k];
         }
     }
-    grid_barrier(P.bar, target, TB, P.xgpu);  // starts with __syncthreads (s_warp reuse is safe)
+    grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);  // starts with __syncthreads (s_warp reuse is safe)
     // own buffer: one per rank (per group when ranks are emulated as groups)
     const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +
                          (size_t)set * 8 * TB;
@@ -316,7 +334,7 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
             *dst = t[0];
         }
     }
-    grid_barrier(P.bar, target, TB, P.xgpu);  // starts with __syncthreads (s_val reuse is safe)
+    grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);  // starts with __syncthreads (s_val reuse is safe)
     if (warp < K) {
         // own buffer: one per rank (per group when ranks are emulated as groups)
         const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +

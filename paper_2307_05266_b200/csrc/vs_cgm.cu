@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
         for (int64_t it = 0; it < P.max_iter; ++it) {
             if (rz < 0.0) { status = 1; sval = rz; sat = it; break; }
             if (rz == 0.0) { conv = true; break; }
+            if (P.xgpu && *P.xflag) { status = 4; sat = it; break; }  // a peer rank never arrived
             const bool first = it == 0;
             const uint64_t t0 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             // ---- P1: d = (z - mu) + beta d_old; d.q
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                     double zn[NS], dn[NS];
 #pragma unroll
                     for (int s = 0; s < NS; ++s) {  // unconditional loads (absent -> own index)
-                        const uint32_t j = nr[s] != ABSENT ? nr[s] : i;
+                        const uint32_t j = (nr[s] != ABSENT && !(P.dbg & 1u)) ? nr[s] : i;
                         zn[s] = z[j];
                         dn[s] = (RC && !first) ? dold[j] : 0.0;
                     }

@@ -42,6 +42,7 @@ struct CgGroup {
     const uint32_t *segstart;
     const int *xp, *xm;
     int nseg;
+    int nstrip;                     // k_pcgs: strips per segment (each at most CG_THREADS DOFs)
     const uint32_t *nbr;            // TIER 3: neighbour ranks [2*dim][m_own] (ABSENT if none);
                                     // TIER 4: int2 x-deltas [m_own], then short2 y-deltas [m_own] (3D)
     // halo: side s = 0 sends the first owned plane to the lower neighbour's
@@ -63,6 +64,8 @@ struct CgParams {
     int block_base;         // global index of this launch's block 0
     int npart;              // ranks whose partial buffers receive this launch's sums
     int xgpu;               // ranks are processes on different GPUs: system-scope barrier
+    volatile int *xflag;    // xgpu: set when a cross-GPU barrier timed out (device memory, read back by the host after a sync)
+    unsigned long long xtimeout_ns;
     int part_self;          // index in part_peer of the first local group's own buffer
     double *part_peer[VS_MAX_SLABS];
     CgOut *out;
@@ -79,6 +82,8 @@ struct CgParams {
     uint32_t cache_slots;
     uint32_t pf_dist;              // L2 prefetch distance in grid strides (0 = off)
     unsigned long long *phase_ns;  // optional [12] accumulators
+    uint32_t dbg;                  // VOXSCHUR_DBG bits (timing experiments only; results are wrong):
+                                   // 1 = P1 gathers read the DOF's own value
 };
 
 
@@ -117,7 +122,8 @@ struct OuterState {
 };
 enum { SO_MEAN, SO_PERM, SO_INIT, SO_ALPHA, SO_BETA };
 enum { Q_DQ, Q_PERM, Q_MU, Q_RZ, Q_ZZ, Q_RR, Q_HOST, Q_COUNT };  // reduction slots (x R slabs)
-void launch_xbar(unsigned *bar, unsigned *bar_base, int nranks, cudaStream_t s);
+void launch_xbar(unsigned *bar, unsigned *bar_base, int nranks, volatile int *xflag, unsigned long long timeout_ns,
+                 cudaStream_t s);
 void launch_outer(int op, OuterState *st, const double *scal, int R, double arg, int64_t k, double eps,
                   int use_prec, double *hist, cudaStream_t s);
 void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s);
@@ -133,7 +139,11 @@ constexpr size_t CG_SMEM_BUDGET = 200 * 1024;  // dynamic smem per block (1 bloc
 // (value 3: 2 is the k_cg1t kernel id in vs_kstat)
 // 4, 5: k_pcgm (vs_cgm.cu), M-scaled over 8-B descriptors: s = M q by
 // recurrence / q = A d recomputed in both passes
-enum CgAlg { CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3, CG_TWO_SUM_MQ = 4, CG_TWO_SUM_MRC = 5 };
+// 6, 7: k_pcgs (vs_cgs.cu), the same two forms on the x-sweep schedule
+enum CgAlg {
+    CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3, CG_TWO_SUM_MQ = 4, CG_TWO_SUM_MRC = 5,
+    CG_SWEEP_MQ = 6, CG_SWEEP_MRC = 7
+};
 struct CgPlan {
     int alg;
     int unroll;   // DOFs per P1 step (k_pcg<QR> only)
@@ -151,6 +161,10 @@ cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &
 // k_pcgm (vs_cgm.cu)
 CgPlan pcgm_plan(int dim, int op, int64_t m, int groups, int device, int alg, int nseg_max, int sms = 0);
 cudaError_t launch_pcgm(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
+// k_pcgs (vs_cgs.cu)
+CgPlan pcgs_plan(int dim, int op, int64_t m, int groups, int device, int alg, int64_t units_max, int sms = 0);
+bool pcgs_fits(int dim, int op, const CgPlan &pl, int device);
+cudaError_t launch_pcgs(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
 void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *first, int *xp, int *xm,
                       cudaStream_t s);
 void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int *xp, const int *xm, uint64_t *desc,

@@ -419,18 +419,31 @@ __global__ void k_outer(int op, OuterState *st, const double *scal, int R, doubl
 // cross-rank barrier for the outer loop: one arrival per rank on the
 // counter the fused CG uses (its base carried in *bar_base).  The ranks are
 // processes on different GPUs, so release/acquire are at system scope.
-__global__ void k_xbar(unsigned *bar, unsigned *bar_base, int nranks) {
+__global__ void k_xbar(unsigned *bar, unsigned *bar_base, int nranks, volatile int *xflag,
+                       unsigned long long timeout_ns) {
     const unsigned target = *bar_base + (unsigned)nranks;
     asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned v;
+    unsigned v, spins = 0;
+    unsigned long long t0 = 0;
     do {
         asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        if (xflag && (++spins & 1023u) == 0) {  // a peer that never arrives must not hang the stream
+            unsigned long long now;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+            if (!t0) t0 = now;
+            if (*xflag) break;
+            if (timeout_ns && now - t0 > timeout_ns) {
+                *xflag = 1;
+                break;
+            }
+        }
     } while ((int)(v - target) < 0);
     asm volatile("fence.acq_rel.sys;" ::: "memory");
     *bar_base = target;
 }
-void launch_xbar(unsigned *bar, unsigned *bar_base, int nranks, cudaStream_t s) {
-    k_xbar<<<1, 1, 0, s>>>(bar, bar_base, nranks);
+void launch_xbar(unsigned *bar, unsigned *bar_base, int nranks, volatile int *xflag, unsigned long long timeout_ns,
+                 cudaStream_t s) {
+    k_xbar<<<1, 1, 0, s>>>(bar, bar_base, nranks, xflag, timeout_ns);
 }
 
 void launch_outer(int op, OuterState *st, const double *scal, int R, double arg, int64_t k, double eps,
