@@ -97,9 +97,7 @@ struct Slab {
     // k_pcgm descriptors (A, S_hat), built on first use
     uint64_t *desc[2] = {nullptr, nullptr};
     uint16_t *cidx[2] = {nullptr, nullptr};
-    uint32_t *segtab[2] = {nullptr, nullptr};  // [nseg + 1] first rank | [nseg] x+ base | [nseg] x- base
-    int nseg[2] = {0, 0};
-    int nstrip[2] = {1, 1};  // k_pcgs: strips per segment
+    int2 *xb[2] = {nullptr, nullptr};  // x+ / x- rank-distance bases per chunk of 1024 ranks
     int64_t n_escape[2] = {0, 0};
     double *u[NU] = {}, *p[NP] = {};
     Geo geo{};
@@ -457,43 +455,29 @@ Status cg_status_to_error(const CgOut &o, int which) {
     return {VS_OK, ""};
 }
 
-inline bool is_sweep_alg(int alg) { return alg == CG_SWEEP_MQ || alg == CG_SWEEP_MRC; }
-inline bool is_m_alg(int alg) { return alg == CG_TWO_SUM_MQ || alg == CG_TWO_SUM_MRC || is_sweep_alg(alg); }
+inline bool is_m_alg(int alg) { return alg == CG_TWO_SUM_MQ || alg == CG_TWO_SUM_MRC; }
 
-// k_pcgm descriptors of one slab and operator (vs_cgm.cu): scan the segment
-// starts and x-bases, fill the empty segments on the host, pack.  Runs once,
-// on the first solve that needs it (synchronises the stream).
+// k_pcgm descriptors of one slab and operator (vs_cgm.cu): the x-bases per
+// chunk of 1024 ranks, then the packed descriptors.  Runs once, on the first
+// solve that needs it.
 void build_descriptors(vs_ctx *c, Slab &S, const CgGroup &G, int op) {
-    const int nseg = (op == 0 ? c->dim : 1) * S.nx;
     const int64_t m = std::max<int64_t>(1, S.m_own[op]);
-    uint32_t *tab = c->alloc<uint32_t>(3 * (size_t)nseg + 1);
-    int *xp = reinterpret_cast<int *>(tab + nseg + 1), *xm = xp + nseg;
-    CK(cudaMemsetAsync(tab, 0xFF, (size_t)(nseg + 1) * 4, c->stream));
-    CK(cudaMemsetAsync(xp, 0x7F, (size_t)2 * nseg * 4, c->stream));  // 0x7F7F7F7F: "no such neighbour here"
-    launch_desc_scan(c->dim, op, G, c->n, c->nw, tab, xp, xm, c->stream);
+    const int64_t nchunk = (m + 1023) / 1024;
+    int2 *xb = c->alloc<int2>(nchunk);
+    CK(cudaMemsetAsync(xb, 0x7F, (size_t)nchunk * sizeof(int2), c->stream));  // 0x7F7F7F7F: "no such neighbour here"
+    launch_desc_scan(c->dim, op, G, c->n, c->nw, xb, c->stream);
     CK(cudaGetLastError());
-    std::vector<uint32_t> first(nseg + 1);
-    CK(cudaMemcpyAsync(first.data(), tab, (size_t)(nseg + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
-    first[nseg] = (uint32_t)S.m_own[op];
-    for (int k = nseg - 1; k >= 0; --k)
-        if (first[k] == 0xFFFFFFFFu) first[k] = first[k + 1];  // empty segment
-    CK(cudaMemcpyAsync(tab, first.data(), (size_t)(nseg + 1) * 4, cudaMemcpyHostToDevice, c->stream));
-    uint32_t lmax = 1;
-    for (int k = 0; k < nseg; ++k) lmax = std::max(lmax, first[k + 1] - first[k]);
-    S.nstrip[op] = (int)((lmax + CG_THREADS - 1) / CG_THREADS);
     S.desc[op] = c->alloc<uint64_t>(m);
     S.cidx[op] = c->alloc<uint16_t>(m);
     unsigned long long *cnt = c->alloc<unsigned long long>(1);
     CK(cudaMemsetAsync(cnt, 0, sizeof *cnt, c->stream));
-    launch_desc_pack(c->dim, op, G, c->n, c->nw, xp, xm, S.desc[op], S.cidx[op], cnt, c->stream);
+    launch_desc_pack(c->dim, op, G, c->n, c->nw, xb, S.desc[op], S.cidx[op], cnt, c->stream);
     CK(cudaGetLastError());
     unsigned long long h = 0;
     CK(cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, c->stream));
-    c->sync();  // `first` must outlive the upload
+    c->sync();
     S.n_escape[op] = (int64_t)h;
-    S.segtab[op] = tab;
-    S.nseg[op] = nseg;
+    S.xb[op] = xb;
     if (!c->ctab[op]) {
         const int count = op == 0 ? 16 : 46656;
         c->ctab[op] = c->alloc<double2>(count);
@@ -561,11 +545,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
             if (!S.desc[op]) build_descriptors(c, S, G, op);
             G.desc = S.desc[op];
             G.cidx = S.cidx[op];
-            G.nseg = S.nseg[op];
-            G.nstrip = S.nstrip[op];
-            G.segstart = S.segtab[op];
-            G.xp = reinterpret_cast<const int *>(S.segtab[op] + S.nseg[op] + 1);
-            G.xm = G.xp + S.nseg[op];
+            G.xb = S.xb[op];
         }
         // k_cg1 buffers (the same slots, paired)
         G.zb[0] = G.z;
@@ -630,8 +610,6 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     // prefetch only where the operator's vectors leave L2 (C1 64^3, L2-resident,
     // on a 46-SM share: A 7.6 -> 8.2 us/it with it); the env value applies as given
     P.pf_dist = (c->pf_forced || m > (int64_t(1) << 20)) ? c->pf_dist : 0;
-    // k_pcgs prefetches whole units: two steps ahead unless VOXSCHUR_PREFETCH says otherwise
-    if (is_sweep_alg((op == 0 ? c->plan_A : c->plan_S).alg)) P.pf_dist = c->pf_forced ? c->pf_dist : 2;
     const CgPlan &pl = op == 0 ? c->plan_A : c->plan_S;
     P.total_blocks = pl.grid * R;          // blocks of every rank
     P.block_base = pl.grid * c->s0;        // global index of this launch's block 0
@@ -646,15 +624,6 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         P.total_blocks = tp.grid;
         P.block_base = 0;
         CK(launch_cg1t(op, tp, P, c->stream));
-    } else if (is_sweep_alg(pl.alg)) {
-        CgPlan ps = pl;  // the unit table of a block's run, sized now that the strips are known
-        int64_t units = 1;
-        for (int q = c->s0; q < c->s1; ++q)
-            units = std::max<int64_t>(units, (int64_t)c->slabs[q].nseg[op] * c->slabs[q].nstrip[op]);
-        ps.smem = (size_t)(units / ps.grid + 2) * 16;
-        if (!pcgs_fits(c->dim, op, ps, c->device))
-            throw Status{VS_ECUDA, "k_pcgs: the unit table does not fit shared memory"};
-        CK(launch_pcgs(c->dim, op, ps, nloc, P, c->stream));
     } else if (is_m_alg(pl.alg)) {
         CK(launch_pcgm(c->dim, op, pl, nloc, P, c->stream));
     } else {
@@ -956,23 +925,22 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     int nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, C->device));
     if (sms > 0 && sms < nsm) nsm = sms;
-    // Two-reduction loop: q by recurrence (k_pcg<QR>, 6 gathers per DOF
-    // instead of 12) for every A- and S_hat-solve, with the packed neighbour
-    // deltas (TIER 4, below) -- single slab and slab groups alike (B200, C2:
-    // A 132.5 -> 97, S_hat 57.3 -> 53.5; C4 512^3: A 1780 -> 1438, S_hat 836
-    // -> 641 us/it, with the carried delta words and the L2 prefetch; C2 on
-    // 1/2/4 slab groups: A 96.8/99.1/99.6, S_hat 53.5/53.4/54.4).
-    // VOXSCHUR_CG=2 forces the reference-order q = A d, =3 the recurrence.
+    // Small operators (at most 4 DOFs per thread): k_cg1, one grid sum per
+    // iteration.  Everything larger, and every slab-decomposed run: k_pcgm in its
+    // qrec form (vs_cgm.cu: two grid sums, M-scaled, 8-B descriptors, 98 B per
+    // DOF-iteration).  B200, us per CG iteration, against the previous default
+    // k_pcg<QR> with packed deltas (124 B): C4 512^3 S_hat 637 -> 510, A 1392 ->
+    // 1113; C2 256^3 S_hat 53.0 -> 50.8, A 96.0 -> 87.3 (profiles/r02f_*, r02g_*).
+    // VOXSCHUR_CG forces a kernel: 1 k_cg1, 2 k_pcg (reference operation order),
+    // 3 k_pcg<QR>, 4 k_pcgm qrec, 5 k_pcgm rc (q recomputed in both passes, 80 B).
     auto pick = [&](int64_t m, int op) {
-        if (force == 6) return (int)CG_SWEEP_MQ;
-        if (force == 7) return (int)CG_SWEEP_MRC;
         if (force == 4) return (int)CG_TWO_SUM_MQ;
         if (force == 5) return (int)CG_TWO_SUM_MRC;
         if (force == 3) return (int)CG_TWO_SUM_QREC;
         if (force == 2) return (int)CG_TWO_SUM;
         if (R == 1 && (force == 1 || (force == 0 && m <= (int64_t)4 * nsm * CG_THREADS)))
             return (int)CG_ONE_SUM;
-        return (int)CG_TWO_SUM_QREC;
+        return (int)CG_TWO_SUM_MQ;
     };
     const char *en = getenv("VOXSCHUR_NBR");
     // VOXSCHUR_NBR=1: TIER 3 (32-bit ranks), =2: TIER 4 (packed deltas)
@@ -987,8 +955,7 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     const int nbr_S = nbr_A;
     auto plan = [&](int op, int64_t m, int nbr_tier) {
         const int alg = pick(m, op);
-        if (is_sweep_alg(alg)) return pcgs_plan(dim, op, m, nloc, C->device, alg, 1, nsm);
-        if (is_m_alg(alg)) return pcgm_plan(dim, op, m, nloc, C->device, alg, (op == 0 ? dim : 1) * (C->n + 2), nsm);
+        if (is_m_alg(alg)) return pcgm_plan(dim, op, m, nloc, C->device, alg, nsm);
         return pcg_plan(dim, op, m, nloc, C->device, alg, nbr_tier, nsm);
     };
     C->plan_A = plan(0, mu_max, nbr_A);

@@ -14,8 +14,9 @@
 //  * one 8-B descriptor per DOF replaces record + deltas (20 B): 18 bits of
 //    integer codes (S_hat: the six 3-bit face codes; A: no-slip code,
 //    neighbour presence, component), the x+- neighbour ranks as 13-bit
-//    residuals against a per-(component, plane) base held in shared memory,
-//    the y+- ranks as 10-bit distances, z+- = i +- 1.  A DOF whose deltas do
+//    residuals against the base of the DOF's 1024-rank chunk (an int2 per
+//    chunk, one warp-uniform load), the y+- ranks as 10-bit distances,
+//    z+- = i +- 1.  A DOF whose deltas do
 //    not fit, or whose z/y neighbour wraps, carries an escape mark and takes
 //    the record + bitmask lookup of vs_cg_common.cuh (about 1 % at 512^3).
 //  * two forms of the operator product:
@@ -66,62 +67,48 @@ __device__ __forceinline__ uint32_t rec_cidx(uint64_t rc) {
     for (int a = 2; a >= 0; --a) v = v * 6 + (uint32_t)rec_pin(rc, a);
     return v;
 }
-template <int DIM, int OP>
-__device__ __forceinline__ int rec_seg(uint64_t rc, int nx) {
-    return (OP == 0 ? rec_comp(rc) * nx : 0) + rec_x(rc);
-}
+constexpr int CHUNK_SHIFT = 10;  // x-bases are kept per chunk of 1024 consecutive ranks
 
 // ---- descriptor build (once per context and operator) --------------------
-// pass 1: first rank of every (component, plane) segment and the smallest
-// x+ / x- rank distance inside it (the bases the residuals are taken from)
+// pass 1: the smallest x+ / x- rank distance inside every chunk (the bases
+// the residuals are taken from)
 template <int DIM, int OP>
-__global__ void k_desc_scan(const CgGroup G, int n, int nw, uint32_t *first, int *xp, int *xm) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = i < G.m_own;
-    int seg = -1, dp = INT_MAX, dm = INT_MAX;
-    if (live) {
+__global__ void k_desc_scan(const CgGroup G, int n, int nw, int2 *xb) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;  // a warp lies inside one chunk
+    int dp = INT_MAX, dm = INT_MAX;
+    if (i < G.m_own) {
         const uint64_t rc = G.rec[i];
         uint32_t nr[2 * DIM];
         neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), nw, n, G.nx, rc, i, nr);
-        seg = rec_seg<DIM, OP>(rc, G.nx);
         if (nr[0] != ABSENT) dp = (int)(nr[0] - i);
         if (nr[1] != ABSENT) dm = (int)(nr[1] - i);
     }
-    // a warp's DOFs are consecutive ranks: almost always one segment
-    const int seg0 = __shfl_sync(~0u, seg, 0);
-    if (__all_sync(~0u, seg == seg0) && seg0 >= 0) {
-        const uint32_t fi = __reduce_min_sync(~0u, i);
-        const int mp = __reduce_min_sync(~0u, dp), mm = __reduce_min_sync(~0u, dm);
-        if ((threadIdx.x & 31) == 0) {
-            atomicMin(first + seg0, fi);
-            if (mp != INT_MAX) atomicMin(xp + seg0, mp);
-            if (mm != INT_MAX) atomicMin(xm + seg0, mm);
-        }
-    } else if (live) {
-        atomicMin(first + seg, i);
-        if (dp != INT_MAX) atomicMin(xp + seg, dp);
-        if (dm != INT_MAX) atomicMin(xm + seg, dm);
+    const int mp = __reduce_min_sync(~0u, dp), mm = __reduce_min_sync(~0u, dm);
+    if ((threadIdx.x & 31) == 0 && i < G.m_own) {
+        int *b = reinterpret_cast<int *>(xb + (i >> CHUNK_SHIFT));
+        if (mp != INT_MAX) atomicMin(b, mp);
+        if (mm != INT_MAX) atomicMin(b + 1, mm);
     }
 }
 // pass 2: pack
 template <int DIM, int OP>
-__global__ void k_desc_pack(const CgGroup G, int n, int nw, const int *xp, const int *xm, uint64_t *desc,
-                            uint16_t *cidx, unsigned long long *n_escape) {
+__global__ void k_desc_pack(const CgGroup G, int n, int nw, const int2 *xb, uint64_t *desc, uint16_t *cidx,
+                            unsigned long long *n_escape) {
     constexpr int NS = 2 * DIM;
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= G.m_own) return;
     const uint64_t rc = G.rec[i];
     uint32_t nr[NS];
     neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), nw, n, G.nx, rc, i, nr);
-    const int seg = rec_seg<DIM, OP>(rc, G.nx);
+    const int2 cb = xb[i >> CHUNK_SHIFT];
     bool esc = false;
     uint64_t ex0 = 0, ex1 = 0, dy0 = 0, dy1 = 0;
     if (nr[0] != ABSENT) {
-        const int64_t e = (int64_t)(int)(nr[0] - i) - xp[seg];
+        const int64_t e = (int64_t)(int)(nr[0] - i) - cb.x;
         if (e < 0 || e >= (int64_t)DX_ESC) esc = true; else ex0 = (uint64_t)e;
     }
     if (nr[1] != ABSENT) {
-        const int64_t e = (int64_t)(int)(nr[1] - i) - xm[seg];
+        const int64_t e = (int64_t)(int)(nr[1] - i) - cb.y;
         if (e < 0 || e > (int64_t)DX_MASK) esc = true; else ex1 = (uint64_t)e;
     }
     if (DIM == 3) {
@@ -160,27 +147,24 @@ __global__ void k_build_ctab(int op, const double2 *sdiag2, const double *diag_c
     ctab[k] = sdiag2[key];
 }
 
-void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *first, int *xp, int *xm,
-                      cudaStream_t s) {
+void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, int2 *xb, cudaStream_t s) {
     if (!G.m_own) return;
     const unsigned nb = (G.m_own + 255) / 256;
     if (dim == 3)
-        op == 0 ? k_desc_scan<3, 0><<<nb, 256, 0, s>>>(G, n, nw, first, xp, xm)
-                : k_desc_scan<3, 1><<<nb, 256, 0, s>>>(G, n, nw, first, xp, xm);
+        op == 0 ? k_desc_scan<3, 0><<<nb, 256, 0, s>>>(G, n, nw, xb) : k_desc_scan<3, 1><<<nb, 256, 0, s>>>(G, n, nw, xb);
     else
-        op == 0 ? k_desc_scan<2, 0><<<nb, 256, 0, s>>>(G, n, nw, first, xp, xm)
-                : k_desc_scan<2, 1><<<nb, 256, 0, s>>>(G, n, nw, first, xp, xm);
+        op == 0 ? k_desc_scan<2, 0><<<nb, 256, 0, s>>>(G, n, nw, xb) : k_desc_scan<2, 1><<<nb, 256, 0, s>>>(G, n, nw, xb);
 }
-void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int *xp, const int *xm, uint64_t *desc,
+void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int2 *xb, uint64_t *desc,
                       uint16_t *cidx, unsigned long long *n_escape, cudaStream_t s) {
     if (!G.m_own) return;
     const unsigned nb = (G.m_own + 255) / 256;
     if (dim == 3)
-        op == 0 ? k_desc_pack<3, 0><<<nb, 256, 0, s>>>(G, n, nw, xp, xm, desc, cidx, n_escape)
-                : k_desc_pack<3, 1><<<nb, 256, 0, s>>>(G, n, nw, xp, xm, desc, cidx, n_escape);
+        op == 0 ? k_desc_pack<3, 0><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape)
+                : k_desc_pack<3, 1><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape);
     else
-        op == 0 ? k_desc_pack<2, 0><<<nb, 256, 0, s>>>(G, n, nw, xp, xm, desc, cidx, n_escape)
-                : k_desc_pack<2, 1><<<nb, 256, 0, s>>>(G, n, nw, xp, xm, desc, cidx, n_escape);
+        op == 0 ? k_desc_pack<2, 0><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape)
+                : k_desc_pack<2, 1><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape);
 }
 void launch_build_ctab(int op, const double2 *sdiag2, const double *diag_code, double2 *ctab, int count,
                        cudaStream_t s) {
@@ -192,7 +176,6 @@ template <int DIM, int OP, bool RC, int NT>
 __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
-    extern __shared__ __align__(16) uint8_t dyn_smem[];  // segment tables
     __shared__ double s_tab[40];
     __shared__ double s_warp[NT / 32][5];
     __shared__ double s_tot[5];
@@ -207,27 +190,19 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
     }
     unsigned gen = __ldcg(P.bar_base);
     __syncthreads();
-    const int nseg = G.nseg;
-    uint32_t *s_seg = reinterpret_cast<uint32_t *>(dyn_smem);  // [nseg + 1] first rank of each segment
-    int *s_xp = reinterpret_cast<int *>(s_seg + nseg + 1);      // [nseg] x+ base
-    int *s_xm = s_xp + nseg;                                    // [nseg] x- base
-    for (int k = threadIdx.x; k <= nseg; k += NT) s_seg[k] = G.segstart[k];
-    for (int k = threadIdx.x; k < nseg; k += NT) {
-        s_xp[k] = G.xp[k];
-        s_xm[k] = G.xm[k];
-    }
-    __syncthreads();
     const Tabs T{s_tab, s_tab + 16, s_tab + 32, P.invS};
     const double2 *sdg = P.sdiag2;
     const double2 *ctab = P.ctab;
     __builtin_assume(__isGlobal(ctab));
     const uint32_t m = G.m_own, m_all = G.m_all;
-    const uint32_t tid = (blockIdx.x % P.bpg) * NT + threadIdx.x;
+    const uint32_t blk0 = (blockIdx.x % P.bpg) * NT;  // first DOF of this block's chunk in stride 0
+    const uint32_t tid = blk0 + threadIdx.x;
     const uint32_t stride = P.bpg * NT;
     double *x = G.x, *z = G.z, *sv = G.q;
     const uint64_t *desc = G.desc;
     const uint16_t *cidx = G.cidx;
     const uint64_t *rec = G.rec;
+    const int2 *xb = G.xb;
     const bool halo = G.zpeer[0] != nullptr;
     __builtin_assume(__isGlobal(x));
     __builtin_assume(__isGlobal(z));
@@ -235,25 +210,53 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
     __builtin_assume(__isGlobal(desc));
     __builtin_assume(__isGlobal(cidx));
     __builtin_assume(__isGlobal(rec));
+    __builtin_assume(__isGlobal(xb));
     const double inv_h = P.inv_h, inv_h2 = P.inv_h2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t pfd = P.pf_dist * stride;
 
-    // descriptor -> record bits and neighbour ranks
-    auto decode = [&](uint64_t d, uint32_t i, int seg, uint64_t &rc, uint32_t (&nr)[NS]) {
+    // descriptor -> record bits, gather indices (an absent neighbour reads the
+    // DOF itself) and the presence mask (A zeroes absent slots)
+    auto decode = [&](uint64_t d, uint32_t i, int2 cb, uint64_t &rc, uint32_t (&j)[NS], uint32_t &pres) {
         const uint32_t fx = (uint32_t)(d >> SH_XP) & DX_MASK;
-        if (fx == DX_ESC) {
+        if (fx == DX_ESC) {  // escape: the record and the bitmask lookups
             rc = rec[i];
+            uint32_t nr[NS];
             neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, i, nr);
+            pres = 0;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                j[s] = nr[s] != ABSENT ? nr[s] : i;
+                pres |= (nr[s] != ABSENT ? 1u : 0u) << s;
+            }
             return;
         }
         rc = desc_rec<OP>(d);
-        nr[0] = rec_has_nb<OP>(rc, 0) ? i + (uint32_t)(s_xp[seg] + (int)fx) : ABSENT;
-        nr[1] = rec_has_nb<OP>(rc, 1) ? i + (uint32_t)(s_xm[seg] + (int)((uint32_t)(d >> SH_XM) & DX_MASK)) : ABSENT;
-        if (DIM == 3) {
-            nr[2] = rec_has_nb<OP>(rc, 2) ? i + ((uint32_t)(d >> SH_YP) & DY_MASK) : ABSENT;
-            nr[3] = rec_has_nb<OP>(rc, 3) ? i - ((uint32_t)(d >> SH_YM) & DY_MASK) : ABSENT;
+        pres = 0;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) pres |= (rec_has_nb<OP>(rc, s) ? 1u : 0u) << s;
+        j[0] = (pres & 1u) ? i + (uint32_t)cb.x + fx : i;
+        j[1] = (pres & 2u) ? i + (uint32_t)cb.y + ((uint32_t)(d >> SH_XM) & DX_MASK) : i;
+        if (DIM == 3) {  // absent y slots carry distance 0
+            j[2] = i + ((uint32_t)(d >> SH_YP) & DY_MASK);
+            j[3] = i - ((uint32_t)(d >> SH_YM) & DY_MASK);
         }
-        nr[NS - 2] = rec_has_nb<OP>(rc, NS - 2) ? i + 1 : ABSENT;
-        nr[NS - 1] = rec_has_nb<OP>(rc, NS - 1) ? i - 1 : ABSENT;
+        j[NS - 2] = i + ((pres >> (NS - 2)) & 1u);
+        j[NS - 1] = i - ((pres >> (NS - 1)) & 1u);
+    };
+    // L2 prefetch of the block's chunk pf_dist strides ahead: one line per lane,
+    // warp w covers half (w & 1) of stream (w >> 1) -- one instruction per thread
+    // and step instead of one per thread and stream (sh = log2 of the element size)
+    auto prefetch_chunk = [&](uint32_t c0, const void *base, int sh) {
+        const uint32_t per_line = 128u >> sh;
+        const uint32_t i = c0 + ((uint32_t)(warp & 1) * 32u + (uint32_t)lane) * per_line;
+        if (base && i < c0 + NT && i < m) {
+            const char *p = reinterpret_cast<const char *>(base) + ((size_t)i << sh);
+            if (P.dbg & 2u)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+            else
+                prefetch_l2(p);
+        }
     };
 
     // ---- setup (krylov.py:102-119): project rhs; r = op(x0) - rhs; z = M^-1 r
@@ -309,47 +312,54 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
     int64_t sat = 0, its = 0;
     bool conv = (ref == 0.0);
     double *dold = G.d0, *dnew = G.d1;
-    __builtin_assume(__isGlobal(dold));
-    __builtin_assume(__isGlobal(dnew));
     unsigned long long ph[4] = {0, 0, 0, 0};
     if (!conv) {
         for (int64_t it = 0; it < P.max_iter; ++it) {
             if (rz < 0.0) { status = 1; sval = rz; sat = it; break; }
             if (rz == 0.0) { conv = true; break; }
             if (P.xgpu && *P.xflag) { status = 4; sat = it; break; }  // a peer rank never arrived
-            const bool first = it == 0;
+            __builtin_assume(__isGlobal(dold));
+            __builtin_assume(__isGlobal(dnew));
             const uint64_t t0 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            // ---- P1: d = (z - mu) + beta d_old; d.q
+            // ---- P1: d = (z - mu) + beta d_old; d.q  (the first iteration,
+            // where d = z - mu and nothing old is read, is its own instantiation)
             double v1[1] = {0.0};
-            {
-                uint64_t dn_ = tid < m ? __ldcs(desc + tid) : 0;  // the next DOF's descriptor, carried across the step
-                int seg = 0;
-                for (uint32_t i = tid; i < m; i += stride) {
-                    const uint32_t ip = i + P.pf_dist * stride;
-                    if (P.pf_dist && ip < m) {  // the own streams pf_dist strides ahead (L2, no registers)
-                        prefetch_l2(z + ip);
-                        prefetch_l2(desc + ip);
-                        if (!first) {
-                            prefetch_l2(dold + ip);
-                            if (!RC) prefetch_l2(sv + ip);
-                        }
-                    }
+            auto pass1 = [&](auto first_c) {
+                constexpr bool first = decltype(first_c)::value;
+                // this warp's prefetch stream: z, descriptors, d_old (, s_old)
+                const int ps = warp >> 1;
+                const void *pfb = ps == 0 ? (const void *)z
+                                : ps == 1 ? (const void *)desc
+                                : (!first && ps == 2) ? (const void *)dold
+                                : (!first && !RC && ps == 3) ? (const void *)sv : nullptr;
+                // the next step's descriptor and chunk base, carried across the step
+                uint64_t dn_ = 0;
+                int2 cbn_ = make_int2(0, 0);
+                if (tid < m) {
+                    dn_ = __ldcs(desc + tid);
+                    cbn_ = __ldg(xb + (tid >> CHUNK_SHIFT));
+                }
+                uint32_t c0 = blk0;
+                for (uint32_t i = tid; i < m; i += stride, c0 += stride) {
+                    if (pfd) prefetch_chunk(c0 + pfd, pfb, 3);
                     const uint64_t d = dn_;
-                    while (seg + 1 < nseg && i >= s_seg[seg + 1]) ++seg;
+                    const int2 cb = cbn_;
                     const double zc = z[i];
                     const double dc = first ? 0.0 : dold[i];
                     const double so = (RC || first) ? 0.0 : sv[i];
                     uint64_t rc;
-                    uint32_t nr[NS];
-                    decode(d, i, seg, rc, nr);
+                    uint32_t j[NS], pres;
+                    decode(d, i, cb, rc, j, pres);
                     double zn[NS], dn[NS];
 #pragma unroll
-                    for (int s = 0; s < NS; ++s) {  // unconditional loads (absent -> own index)
-                        const uint32_t j = (nr[s] != ABSENT && !(P.dbg & 1u)) ? nr[s] : i;
-                        zn[s] = z[j];
-                        dn[s] = (RC && !first) ? dold[j] : 0.0;
+                    for (int s = 0; s < NS; ++s) {
+                        zn[s] = z[j[s]];
+                        dn[s] = (RC && !first) ? dold[j[s]] : 0.0;
                     }
-                    if (i + stride < m) dn_ = __ldcs(desc + i + stride);
+                    if (i + stride < m) {
+                        dn_ = __ldcs(desc + i + stride);
+                        cbn_ = __ldg(xb + ((i + stride) >> CHUNK_SHIFT));
+                    }
                     const double zp = PROJ ? __dsub_rn(zc, mu) : zc;
                     const double di = first ? zp : __dadd_rn(zp, __dmul_rn(beta, dc));
                     double vn[NS];
@@ -358,8 +368,8 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                         double zj = PROJ ? __dsub_rn(zn[s], mu) : zn[s];
                         if (RC && !first) zj = __dadd_rn(zj, __dmul_rn(beta, dn[s]));
                         // A needs 0.0 at absent slots (left fold); S_hat's absent faces
-                        // carry weight 0.0 (op_value), so the clamped value is harmless
-                        vn[s] = (OP == 0 && nr[s] == ABSENT) ? 0.0 : zj;
+                        // carry weight 0.0 (op_value), so the DOF's own value is harmless
+                        vn[s] = (OP == 0 && !((pres >> s) & 1u)) ? 0.0 : zj;
                     }
                     dnew[i] = di;
                     if (RC) {
@@ -381,7 +391,11 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                         if (PROJ) zc = __dsub_rn(zc, mu);
                         dnew[i] = first ? zc : __dadd_rn(zc, __dmul_rn(beta, dold[i]));
                     }
-            }
+            };
+            if (it == 0)
+                pass1(std::true_type{});
+            else
+                pass1(std::false_type{});
             const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
             grid_sum<1, false, NT>(v1, 2, P, gen, s_val, s_tot);
             const uint64_t t2 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
@@ -395,29 +409,34 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
 #pragma unroll
             for (int s = 0; s < KL; ++s) v[s] = 0.0;
             if (RC) {
-                uint64_t dn_ = tid < m ? __ldcs(desc + tid) : 0;
-                int seg = 0;
-                for (uint32_t i = tid; i < m; i += stride) {
-                    const uint32_t ip = i + P.pf_dist * stride;
-                    if (P.pf_dist && ip < m) {
-                        prefetch_l2(dnew + ip);
-                        prefetch_l2(x + ip);
-                        prefetch_l2(z + ip);
-                        prefetch_l2(desc + ip);
-                    }
+                const int ps = warp >> 1;
+                const void *pfb = ps == 0 ? (const void *)dnew : ps == 1 ? (const void *)desc
+                                : ps == 2 ? (const void *)x : ps == 3 ? (const void *)z : nullptr;
+                uint64_t dn_ = 0;
+                int2 cbn_ = make_int2(0, 0);
+                if (tid < m) {
+                    dn_ = __ldcs(desc + tid);
+                    cbn_ = __ldg(xb + (tid >> CHUNK_SHIFT));
+                }
+                uint32_t c0 = blk0;
+                for (uint32_t i = tid; i < m; i += stride, c0 += stride) {
+                    if (pfd) prefetch_chunk(c0 + pfd, pfb, 3);
                     const uint64_t d = dn_;
-                    while (seg + 1 < nseg && i >= s_seg[seg + 1]) ++seg;
+                    const int2 cb = cbn_;
                     const double di = dnew[i], xo = x[i], zo = z[i];
                     uint64_t rc;
-                    uint32_t nr[NS];
-                    decode(d, i, seg, rc, nr);
+                    uint32_t j[NS], pres;
+                    decode(d, i, cb, rc, j, pres);
                     double vn[NS];
 #pragma unroll
                     for (int s = 0; s < NS; ++s) {
-                        const double dj = dnew[nr[s] != ABSENT ? nr[s] : i];
-                        vn[s] = (OP == 0 && nr[s] == ABSENT) ? 0.0 : dj;
+                        const double dj = dnew[j[s]];
+                        vn[s] = (OP == 0 && !((pres >> s) & 1u)) ? 0.0 : dj;
                     }
-                    if (i + stride < m) dn_ = __ldcs(desc + i + stride);
+                    if (i + stride < m) {
+                        dn_ = __ldcs(desc + i + stride);
+                        cbn_ = __ldg(xb + ((i + stride) >> CHUNK_SHIFT));
+                    }
                     double inv, dg;
                     inv_diag<OP>(rc, T, sdg, inv, dg);
                     const double qi = op_value<DIM, OP>(rc, di, vn, T, inv_h, inv_h2);
@@ -435,9 +454,12 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                     }
                 }
             } else {
+                // a pure stream, not issue-bound: every thread prefetches its own next
+                // elements (B200, C4 512^3: the one-line-per-lane bursts of P1 cost this
+                // pass 70 us/it -- hints issued in bursts are dropped under load)
                 for (uint32_t i = tid; i < m; i += stride) {
-                    const uint32_t ip = i + P.pf_dist * stride;
-                    if (P.pf_dist && ip < m) {
+                    const uint32_t ip = i + pfd;
+                    if (pfd && ip < m) {
                         prefetch_l2(dnew + ip);
                         prefetch_l2(sv + ip);
                         prefetch_l2(x + ip);
@@ -518,8 +540,8 @@ static const void *pcgm_fn(int dim, int op, bool rc, int nt) {
     return op == 0 ? pcgm_fn_t<2, 0>(rc, nt) : pcgm_fn_t<2, 1>(rc, nt);
 }
 
-// Plan: one block per SM (per group), segment tables in dynamic smem.
-CgPlan pcgm_plan(int dim, int op, int64_t m, int groups, int device, int alg, int nseg_max, int sms) {
+// Plan: one block per SM (per group); no dynamic shared memory.
+CgPlan pcgm_plan(int dim, int op, int64_t m, int groups, int device, int alg, int sms) {
     CgPlan pl{};
     pl.alg = alg;
     pl.unroll = 1;
@@ -532,8 +554,7 @@ CgPlan pcgm_plan(int dim, int op, int64_t m, int groups, int device, int alg, in
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     if (sms > 0 && sms < nsm) nsm = sms;
     const void *fn = pcgm_fn(dim, op, alg == CG_TWO_SUM_MRC, nt);
-    pl.smem = (size_t)(3 * nseg_max + 1) * 4;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    pl.smem = 0;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, pl.smem);
     if (per_sm < 1) per_sm = 1;

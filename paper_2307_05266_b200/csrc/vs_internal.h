@@ -35,14 +35,11 @@ struct CgGroup {
     const double *rhs, *x0;
     double *x, *r, *z, *d0, *d1, *q;
     double *zb[2], *ub[2], *sb[2];  // k_cg1: double-buffered zr = M r, u = M A zr, s = M q
-    // k_pcgm (vs_cgm.cu): 8-B descriptors, 2-B code indices and the per-segment
-    // tables (segment = (component, x-plane): first rank, x+ base, x- base)
+    // k_pcgm (vs_cgm.cu): 8-B descriptors, 2-B code indices and the x+ / x-
+    // rank-distance bases per chunk of 1024 ranks
     const uint64_t *desc;
     const uint16_t *cidx;
-    const uint32_t *segstart;
-    const int *xp, *xm;
-    int nseg;
-    int nstrip;                     // k_pcgs: strips per segment (each at most CG_THREADS DOFs)
+    const int2 *xb;
     const uint32_t *nbr;            // TIER 3: neighbour ranks [2*dim][m_own] (ABSENT if none);
                                     // TIER 4: int2 x-deltas [m_own], then short2 y-deltas [m_own] (3D)
     // halo: side s = 0 sends the first owned plane to the lower neighbour's
@@ -139,11 +136,7 @@ constexpr size_t CG_SMEM_BUDGET = 200 * 1024;  // dynamic smem per block (1 bloc
 // (value 3: 2 is the k_cg1t kernel id in vs_kstat)
 // 4, 5: k_pcgm (vs_cgm.cu), M-scaled over 8-B descriptors: s = M q by
 // recurrence / q = A d recomputed in both passes
-// 6, 7: k_pcgs (vs_cgs.cu), the same two forms on the x-sweep schedule
-enum CgAlg {
-    CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3, CG_TWO_SUM_MQ = 4, CG_TWO_SUM_MRC = 5,
-    CG_SWEEP_MQ = 6, CG_SWEEP_MRC = 7
-};
+enum CgAlg { CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3, CG_TWO_SUM_MQ = 4, CG_TWO_SUM_MRC = 5 };
 struct CgPlan {
     int alg;
     int unroll;   // DOFs per P1 step (k_pcg<QR> only)
@@ -159,15 +152,10 @@ void launch_build_nbr(int dim, int op, const CgGroup &G, int n, int nw, uint32_t
                       int tier = 3);
 cudaError_t launch_pcg(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
 // k_pcgm (vs_cgm.cu)
-CgPlan pcgm_plan(int dim, int op, int64_t m, int groups, int device, int alg, int nseg_max, int sms = 0);
+CgPlan pcgm_plan(int dim, int op, int64_t m, int groups, int device, int alg, int sms = 0);
 cudaError_t launch_pcgm(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
-// k_pcgs (vs_cgs.cu)
-CgPlan pcgs_plan(int dim, int op, int64_t m, int groups, int device, int alg, int64_t units_max, int sms = 0);
-bool pcgs_fits(int dim, int op, const CgPlan &pl, int device);
-cudaError_t launch_pcgs(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
-void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, uint32_t *first, int *xp, int *xm,
-                      cudaStream_t s);
-void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int *xp, const int *xm, uint64_t *desc,
+void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, int2 *xb, cudaStream_t s);
+void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int2 *xb, uint64_t *desc,
                       uint16_t *cidx, unsigned long long *n_escape, cudaStream_t s);
 void launch_build_ctab(int op, const double2 *sdiag2, const double *diag_code, double2 *ctab, int count,
                        cudaStream_t s);
