@@ -339,13 +339,33 @@ def run_ours(a):
     kw["max_iter"] = cap if cap is not None else spec.max_iter
     cfgs = [vx.SchurConfig(prec=p, **kw) for p in precs]
 
+    def all_ok(ok):
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=f"cuda:{dev}")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        return bool(int(flag.item()))
+
     def build():
+        nonlocal slabbed
         if slabbed:
-            ss = [vx.assemble(grid, 0, check_connectivity=spec.check_connectivity, device=dev,
-                              rank=rank, nranks=world) for _ in cfgs]
-            for s in ss:
-                vx.connect_ranks(s)
-            return ss
+            # every collective below is entered by every rank, whatever failed locally
+            ss = None
+            try:
+                ss = [vx.assemble(grid, 0, check_connectivity=spec.check_connectivity, device=dev,
+                                  rank=rank, nranks=world) for _ in cfgs]
+            except Exception as e:  # noqa: BLE001
+                print(f"rank {rank}: slab context failed: {type(e).__name__}: {e}", file=sys.stderr)
+            if all_ok(ss is not None):
+                ok = True
+                try:
+                    for s in ss:
+                        vx.connect_ranks(s)
+                except Exception as e:  # noqa: BLE001
+                    print(f"rank {rank}: connect_ranks failed: {type(e).__name__}: {e}", file=sys.stderr)
+                    ok = False
+                if all_ok(ok):
+                    return ss
+            slabbed = False  # every rank: independent replicas instead
+            del ss
         return [vx.assemble(grid, 0, check_connectivity=spec.check_connectivity, device=dev) for _ in cfgs]
 
     # one system (context: work vectors + stream) per preconditioner, so the
@@ -408,7 +428,30 @@ def run_ours(a):
 
     # warm-up 1 runs the solves one after another on the whole device.  With
     # two small solves (C1), untimed tuning steps then pick the SM split.
-    seq = one_step(None)
+    slab_error = None
+    if slabbed:
+        # the slab transport (CUDA IPC + cross-GPU barriers) has never run on
+        # hardware: if any rank fails to build or to finish its first step (a
+        # barrier that times out raises instead of hanging), every rank falls
+        # back to independent replicas and the line says so
+        failed = 0
+        try:
+            seq = one_step(None)
+        except Exception as e:  # noqa: BLE001
+            failed, slab_error = 1, f"{type(e).__name__}: {e}"
+        flag = torch.tensor([failed], dtype=torch.int32, device=f"cuda:{dev}")
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        if int(flag.item()):
+            slab_error = slab_error or "another rank failed"
+            print(f"rank {rank}: slab decomposition failed ({slab_error}); falling back to replicas",
+                  file=sys.stderr)
+            slabbed = False
+            del systems
+            systems = build()
+            sys_ = systems[0]
+            seq = one_step(None)
+    else:
+        seq = one_step(None)
     shares, tuning = None, []
     if len(cfgs) == 2 and small and not a.sequential and not slabbed:
         total = systems[0].sms
@@ -509,6 +552,8 @@ def run_ours(a):
         with open(tp) as f:
             tj = json.load(f)
         traffic = tj.get(a.config, {}).get(kname)
+        if isinstance(traffic, dict):  # measured DRAM bytes per DOF-iteration -> per launch of this run
+            traffic = traffic["bytes_per_dof_iter"] * dof_k / max(1, l_k)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "kernel": f"{kname} (fused persistent PCG, one launch per inner solve)",
@@ -547,6 +592,7 @@ def run_ours(a):
             "higher_is_better": True, "scaling": "strong" if slabbed else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": cfg_obj,
             "parallelism": (f"xslab{world}" if slabbed else (f"replicas{world}" if world > 1 else "single")),
+            "slab_fallback": slab_error,
             "sm_shares": {r["prec"]: r["sms"] for r in last}, "sm_split_tuning_ms": tuning,
             "hbm_gbs_algorithmic": hbm_alg,
             "setup_s": {"generate_mask": t_gen, "assemble": t_asm},
