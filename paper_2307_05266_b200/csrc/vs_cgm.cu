@@ -344,6 +344,10 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                     if (pfd) prefetch_chunk(c0 + pfd, pfb, 3);
                     const uint64_t d = dn_;
                     const int2 cb = cbn_;
+                    if (i + stride < m) {  // issued first: a whole step to arrive
+                        dn_ = __ldcs(desc + i + stride);
+                        cbn_ = __ldg(xb + ((i + stride) >> CHUNK_SHIFT));
+                    }
                     const double zc = z[i];
                     const double dc = first ? 0.0 : dold[i];
                     const double so = (RC || first) ? 0.0 : sv[i];
@@ -355,10 +359,6 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                     for (int s = 0; s < NS; ++s) {
                         zn[s] = z[j[s]];
                         dn[s] = (RC && !first) ? dold[j[s]] : 0.0;
-                    }
-                    if (i + stride < m) {
-                        dn_ = __ldcs(desc + i + stride);
-                        cbn_ = __ldg(xb + ((i + stride) >> CHUNK_SHIFT));
                     }
                     const double zp = PROJ ? __dsub_rn(zc, mu) : zc;
                     const double di = first ? zp : __dadd_rn(zp, __dmul_rn(beta, dc));
@@ -423,6 +423,10 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                     if (pfd) prefetch_chunk(c0 + pfd, pfb, 3);
                     const uint64_t d = dn_;
                     const int2 cb = cbn_;
+                    if (i + stride < m) {
+                        dn_ = __ldcs(desc + i + stride);
+                        cbn_ = __ldg(xb + ((i + stride) >> CHUNK_SHIFT));
+                    }
                     const double di = dnew[i], xo = x[i], zo = z[i];
                     uint64_t rc;
                     uint32_t j[NS], pres;
@@ -432,10 +436,6 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                     for (int s = 0; s < NS; ++s) {
                         const double dj = dnew[j[s]];
                         vn[s] = (OP == 0 && !((pres >> s) & 1u)) ? 0.0 : dj;
-                    }
-                    if (i + stride < m) {
-                        dn_ = __ldcs(desc + i + stride);
-                        cbn_ = __ldg(xb + ((i + stride) >> CHUNK_SHIFT));
                     }
                     double inv, dg;
                     inv_diag<OP>(rc, T, sdg, inv, dg);
@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                 // a pure stream, not issue-bound: every thread prefetches its own next
                 // elements (B200, C4 512^3: the one-line-per-lane bursts of P1 cost this
                 // pass 70 us/it -- hints issued in bursts are dropped under load)
+                uint32_t cin_ = tid < m ? (uint32_t)__ldcs(cidx + tid) : 0u;  // the next step's code index, carried
                 for (uint32_t i = tid; i < m; i += stride) {
                     const uint32_t ip = i + pfd;
                     if (pfd && ip < m) {
@@ -465,9 +466,10 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                         prefetch_l2(x + ip);
                         prefetch_l2(z + ip);
                     }
+                    const uint32_t ci = cin_;
+                    const double2 t = __ldg(ctab + (OP == 0 ? (ci & 0xFFu) : ci));  // no load ahead of this lookup
+                    if (i + stride < m) cin_ = (uint32_t)__ldcs(cidx + i + stride);
                     const double di = dnew[i], si = sv[i], xo = x[i], zo = z[i];
-                    const uint32_t ci = __ldcs(cidx + i);
-                    const double2 t = __ldg(ctab + (OP == 0 ? (ci & 0xFFu) : ci));
                     const double xi = __dsub_rn(xo, __dmul_rn(alpha, di));
                     const double zi = __dsub_rn(zo, __dmul_rn(alpha, si));
                     x[i] = xi;
