@@ -176,7 +176,7 @@ template <int DIM, int OP, bool RC, int NT>
 __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
-    __shared__ double s_tab[40];
+    __shared__ double s_tab[48];  // [40..47]: S_hat face weights times inv_h^2 (qrec form)
     __shared__ double s_warp[NT / 32][5];
     __shared__ double s_tot[5];
     __shared__ __align__(16) double s_val[4][NT];  // grid_sum staging
@@ -186,11 +186,15 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
     if (threadIdx.x < 16) {
         s_tab[threadIdx.x] = P.diag_code[threadIdx.x];
         s_tab[16 + threadIdx.x] = P.inv_code[threadIdx.x];
-        if (threadIdx.x < 8) s_tab[32 + threadIdx.x] = P.invA_enc[threadIdx.x];
+        if (threadIdx.x < 8) {
+            s_tab[32 + threadIdx.x] = P.invA_enc[threadIdx.x];
+            s_tab[40 + threadIdx.x] = __dmul_rn(P.invA_enc[threadIdx.x], P.inv_h2);
+        }
     }
     unsigned gen = __ldcg(P.bar_base);
     __syncthreads();
     const Tabs T{s_tab, s_tab + 16, s_tab + 32, P.invS};
+    const double *wS = s_tab + 40;
     const double2 *sdg = P.sdiag2;
     const double2 *ctab = P.ctab;
     __builtin_assume(__isGlobal(ctab));
@@ -365,7 +369,8 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                     double vn[NS];
 #pragma unroll
                     for (int s = 0; s < NS; ++s) {
-                        double zj = PROJ ? __dsub_rn(zn[s], mu) : zn[s];
+                        // qrec S_hat: the stencil takes differences only, so mu cancels
+                        double zj = (PROJ && RC) ? __dsub_rn(zn[s], mu) : zn[s];
                         if (RC && !first) zj = __dadd_rn(zj, __dmul_rn(beta, dn[s]));
                         // A needs 0.0 at absent slots (left fold); S_hat's absent faces
                         // carry weight 0.0 (op_value), so the DOF's own value is harmless
@@ -378,7 +383,22 @@ __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
                     } else {
                         double inv, dg;
                         inv_diag<OP>(rc, T, sdg, inv, dg);
-                        const double mw = __dmul_rn(op_value<DIM, OP>(rc, zp, vn, T, inv_h, inv_h2), inv);
+                        double w;
+                        if (OP == 1) {
+                            // S_hat z = sum_a (z_i - z_in) W_in - (z_out - z_i) W_out with the
+                            // face weights pre-multiplied by inv_h^2 (schur.py:234-240 up to
+                            // rounding: this form is M-scaled, not bitwise the reference's)
+                            w = 0.0;
+#pragma unroll
+                            for (int a = 0; a < DIM; ++a) {
+                                const double wi = __dmul_rn(__dsub_rn(zc, vn[2 * a + 1]), wS[rec_pin(rc, a)]);
+                                const double wo = __dmul_rn(__dsub_rn(vn[2 * a], zc), wS[rec_pout(rc, a)]);
+                                w = __dadd_rn(w, __dsub_rn(wi, wo));
+                            }
+                        } else {
+                            w = op_value<DIM, OP>(rc, zp, vn, T, inv_h, inv_h2);
+                        }
+                        const double mw = __dmul_rn(w, inv);
                         const double si = first ? mw : __dadd_rn(mw, __dmul_rn(beta, so));
                         sv[i] = si;
                         v1[0] = __dadd_rn(v1[0], __dmul_rn(di, __dmul_rn(dg, si)));
