@@ -506,7 +506,7 @@ def run_ours(a):
 
     # e2e through the public API with host buffers (H2D mask, D2H p, u):
     # a bounded number of steps (each repeats the assemble)
-    n_e2e = max(1, min(a.steps, 3 if not small else a.steps))
+    n_e2e = 0 if a.no_e2e else max(1, min(a.steps, 3 if not small else a.steps))
     e2e_t, e2e_cells, h2d, d2h = 0.0, 0, 0, 0
     for _ in range(n_e2e):
         if flush is not None:
@@ -523,7 +523,7 @@ def run_ours(a):
         print(f"e2e step {1e3 * dt:.1f} ms", file=sys.stderr)
         h2d += grid.fluid.size * len(cfgs)  # uint8 mask, one upload per system
         del sy2
-    e2e = {"value": e2e_cells / e2e_t / 1e9, "unit": "Gcell/s",
+    e2e = None if not n_e2e else {"value": e2e_cells / e2e_t / 1e9, "unit": "Gcell/s",
            "h2d_bytes_per_step": h2d // n_e2e, "d2h_bytes_per_step": d2h // n_e2e,
            "ms_per_step": 1e3 * e2e_t / n_e2e, "steps": n_e2e,
            "includes": "assemble of one system per solve (connectivity check + H2D mask + device "
@@ -618,6 +618,7 @@ def main():
                     help="outer-iteration cap of a step (default: the workload's; C4: 1)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end steps (long evidence runs)")
     ap.add_argument("--sequential", action="store_true",
                     help="run the step's solves one after another on the whole device")
     ap.add_argument("--replicas", action="store_true",

@@ -955,7 +955,16 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     const int nbr_S = nbr_A;
     auto plan = [&](int op, int64_t m, int nbr_tier) {
         const int alg = pick(m, op);
-        if (is_m_alg(alg)) return pcgm_plan(dim, op, m, nloc, C->device, alg, nsm);
+        if (is_m_alg(alg)) {
+            // an operator whose neighbour ranks fit the shared-memory DOF cache (TIER 2:
+            // no descriptor stream, no rank arithmetic) keeps k_pcg<QR> -- e.g. the C1
+            // A-solve on a 46-SM share: 14.9 vs 17.9 us/it with k_pcgm (B200)
+            if (force == 0) {
+                const CgPlan q = pcg_plan(dim, op, m, nloc, C->device, CG_TWO_SUM_QREC, 0, nsm);
+                if (q.tier == 2) return q;
+            }
+            return pcgm_plan(dim, op, m, nloc, C->device, alg, nsm);
+        }
         return pcg_plan(dim, op, m, nloc, C->device, alg, nbr_tier, nsm);
     };
     C->plan_A = plan(0, mu_max, nbr_A);
