@@ -10,6 +10,7 @@ usage: python tools/config_report.py [keys...] [--cap-c4 N] > profiles/r01_confi
 """
 import json
 import os
+import subprocess
 import sys
 import time
 
@@ -49,6 +50,31 @@ def main():
     if "--cap-c4" in sys.argv:
         cap = int(sys.argv[sys.argv.index("--cap-c4") + 1])
     keys = args or ["C0", "C1", "C2", "C3s2", "C3s4", "C3s8", "C3s16", "C3s32", "C3c", "C4"]
+    # clocks and throttle reasons sampled over the whole run (one record at the end)
+    smi = None
+    try:
+        smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                                "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                                "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "500",
+                                "-i", "0"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+    except OSError:
+        pass
+    try:
+        run(keys, cap)
+    finally:
+        if smi is not None:
+            smi.terminate()
+            out = smi.communicate()[0].splitlines()
+            sm = sorted(float(ln.split(",")[0]) for ln in out if ln.strip())
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            reasons = sorted({nm for ln in out for nm, v in zip(names, ln.split(",")[2:6]) if v.strip().startswith("Active")})
+            print(json.dumps({"clocks": {"samples": len(sm), "sm_mhz_median": sm[len(sm) // 2] if sm else None,
+                                         "sm_mhz_min": sm[0] if sm else None,
+                                         "sm_max_mhz": float(out[0].split(",")[1]) if out else None,
+                                         "reasons": reasons}}), flush=True)
+
+
+def run(keys, cap):
     for key in keys:
         spec = configs.CONFIGS[key]
         t0 = time.perf_counter()
@@ -84,6 +110,16 @@ def main():
                 line["k_rel_err"] = abs(rep.k_value - kk) / kk
             if capped and rep.iters_outer:
                 line["ms_per_outer"] = rep.device_ms / rep.iters_outer
+            if rep.iters_outer == 0 and rep.cond_est_outer is None:
+                # flow-aligned prisms: g == 0, the reference reports no estimate
+                # (schur.py:359-362); the labelled supplement of SURVEY App. B-4
+                try:
+                    est = vx.supplementary_condition_estimate(s, cfg, seed=0)
+                    line["supplementary"] = {k: est[k] for k in ("label", "seed", "iters_outer", "converged",
+                                                                 "cond_est_outer", "lambda_min_est",
+                                                                 "lambda_max_est", "inner_iter_totals", "device_ms")}
+                except RuntimeError as e:
+                    line["supplementary"] = {"error": str(e)}
             print(json.dumps(line), flush=True)
         del s
 
