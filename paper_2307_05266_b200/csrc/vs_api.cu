@@ -259,12 +259,16 @@ struct vs_ctx {
     double dot(int space, int a, int b) { return reduce(space, 1, a, b); }
     double sum(int space, int a) { return reduce(space, 0, a, -1); }
     double mean(int space, int a) { return sum(space, a) / (double)(space == 0 ? m_u : m_p); }
+    // outer-loop gate: while vs_solve_schur enqueues several outer iterations ahead of
+    // the host, every kernel of the loop gets &ost->stop and turns into a no-op once the
+    // outer PCG has converged or failed; nullptr everywhere else
+    const int *gate = nullptr;
     void vec(int space, int kind, int out, int a, int b, double sc, const double *sp = nullptr) {
         for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
             double **v = space == 0 ? S.u : S.p;
             launch_vec(kind, out < 0 ? nullptr : v[out], v[a], b < 0 ? nullptr : v[b], sc, sp, S.m_own[space],
-                       stream);
+                       stream, gate);
             ++launches;
         }
     }
@@ -277,7 +281,8 @@ struct vs_ctx {
             const double *pb = b < 0 ? nullptr : (space == 0 ? S.u[b] : S.p[b]);
             int64_t off = 0, m = S.m_own[space];
             if (lo_fam >= 0) { off = S.own_off[lo_fam]; m = S.own[lo_fam]; }
-            launches += launch_reduce(kind, pa + off, pb ? pb + off : nullptr, m, red_part, scal + q * R + s, stream);
+            launches += launch_reduce(kind, pa + off, pb ? pb + off : nullptr, m, red_part, scal + q * R + s, stream,
+                                      gate);
         }
     }
     void copy(int space, int dst, int src) {
@@ -352,7 +357,7 @@ struct vs_ctx {
         halo(1, p_in);
         for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
-            launch_apply_grad(S.geo, S.vrec, S.p[p_in], S.u[u_out], S.m_own[0], inv_h, stream);
+            launch_apply_grad(S.geo, S.vrec, S.p[p_in], S.u[u_out], S.m_own[0], inv_h, stream, gate);
             ++launches;
         }
     }
@@ -360,7 +365,7 @@ struct vs_ctx {
         halo(0, u_in);
         for (int s = s0; s < s1; ++s) {
             Slab &S = slabs[s];
-            launch_apply_div(S.geo, S.prec, S.u[u_in], S.p[p_out], S.m_own[1], inv_h, stream);
+            launch_apply_div(S.geo, S.prec, S.u[u_in], S.p[p_out], S.m_own[1], inv_h, stream, gate);
             ++launches;
         }
     }
@@ -589,6 +594,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.part_self = c->mp() ? c->rank : 0;
     for (int r = 0; r < c->npart; ++r) P.part_peer[r] = c->part_peer[r];
     P.phase_ns = c->phase_ns;
+    P.gate = c->gate;
     if (const char *e = getenv("VOXSCHUR_DBG")) P.dbg = (uint32_t)atoi(e);
     P.out = c->cglog + li;
     P.tol = eps;
@@ -694,7 +700,10 @@ void reset_stats(vs_ctx *c) {
 template <class F>
 int guarded(vs_ctx *c, F &&f) {
     try {
-        if (c) CK(cudaSetDevice(c->device));
+        if (c) {
+            CK(cudaSetDevice(c->device));
+            c->gate = nullptr;  // a call that failed inside a gated batch must not gate this one
+        }
         f();
         return VS_OK;
     } catch (const Status &s) {
@@ -1521,13 +1530,13 @@ static int solve_schur_impl(vs_ctx *c, const vs_schur_cfg *cfg, const double *g_
         auto perm = [&](int slot, int64_t k) {  // schur.py:288 -> hist perm[k + 1]
             c->reduce_dev(0, 0, slot, -1, Q_PERM, c->flow_dir);
             c->publish(Q_PERM, Q_PERM + 1);
-            launch_outer(SO_PERM, c->ost, c->scal, R, cfg->h_pow_dim, k, 0, 0, c->hist, s);
+            launch_outer(SO_PERM, c->ost, c->scal, R, cfg->h_pow_dim, k, 0, 0, c->hist, s, c->gate);
             ++c->launches;
         };
         auto mean_into_mu = [&](int slot) {
             c->reduce_dev(1, 0, slot, -1, Q_MU);
             c->publish(Q_MU, Q_MU + 1);
-            launch_outer(SO_MEAN, c->ost, c->scal, R, (double)c->m_p, 0, 0, 0, c->hist, s);
+            launch_outer(SO_MEAN, c->ost, c->scal, R, (double)c->m_p, 0, 0, 0, c->hist, s, c->gate);
             ++c->launches;
         };
         int64_t tot_vel = 0, tot_pre = 0;
@@ -1613,7 +1622,7 @@ static int solve_schur_impl(vs_ctx *c, const vs_schur_cfg *cfg, const double *g_
         c->vec(1, 4, P_R, P_Q, P_B, 0.0);  // r = op(x) - rhs
         outer_prec(P_R, P_Z);
         norms();
-        launch_outer(SO_INIT, c->ost, c->scal, R, 0, 0, cfg->eps_S, use_prec, c->hist, s);
+        launch_outer(SO_INIT, c->ost, c->scal, R, 0, 0, cfg->eps_S, use_prec, c->hist, s, c->gate);
         ++c->launches;
         c->copy(1, P_D, P_Z);
         {
@@ -1637,11 +1646,23 @@ static int solve_schur_impl(vs_ctx *c, const vs_schur_cfg *cfg, const double *g_
                 throw Status{VS_ERUNTIME, buf};
             }
         }
+        // Small operators: an outer iteration is a few hundred microseconds of kernels,
+        // and a host round trip per iteration (read the state, enqueue the next ~20
+        // launches) leaves the GPU idle for about a third as long.  There, `batch`
+        // iterations are enqueued per synchronisation, every kernel gated on the
+        // device-side stop flag (set with `converged` / `status` by k_outer), so the
+        // iterations enqueued past convergence are no-ops and the results are the ones of
+        // the one-by-one loop.  VOXSCHUR_OUTER_BATCH overrides (1 = one by one).
+        int batch = (R == 1 && !c->mp() && !c->use_tile[0] && !c->use_tile[1] && c->m_u <= ((int64_t)1 << 21)) ? 4 : 1;
+        if (const char *eb = getenv("VOXSCHUR_OUTER_BATCH")) batch = std::max(1, std::min(atoi(eb), GROUP_RING / 2));
+        if (R > 1 || c->mp()) batch = 1;  // halo copies and cross-rank barriers are not gated
+        int in_batch = 0;
         for (int64_t k = 0; k < cfg->max_iter && !c->h_ost->converged; ++k) {
+            c->gate = batch > 1 ? &c->ost->stop : nullptr;
             outer_op(P_D, P_Q);
             c->reduce_dev(1, 1, P_D, P_Q, Q_DQ);
             c->publish(Q_DQ, Q_DQ + 1);
-            launch_outer(SO_ALPHA, c->ost, c->scal, R, 0, k, 0, 0, c->hist, s);  // alpha = rz / d'q
+            launch_outer(SO_ALPHA, c->ost, c->scal, R, 0, k, 0, 0, c->hist, s, c->gate);  // alpha = rz / d'q
             ++c->launches;
             c->vec(1, 1, -1, P_X, P_D, 0.0, alpha);    // x -= alpha d
             c->vec(1, 1, -1, P_R, P_Q, 0.0, alpha);    // r -= alpha q
@@ -1649,11 +1670,16 @@ static int solve_schur_impl(vs_ctx *c, const vs_schur_cfg *cfg, const double *g_
             perm(U_ITER, k);
             outer_prec(P_R, P_Z);
             norms();
-            launch_outer(SO_BETA, c->ost, c->scal, R, 0, k, cfg->eps_S, use_prec, c->hist, s);
+            launch_outer(SO_BETA, c->ost, c->scal, R, 0, k, cfg->eps_S, use_prec, c->hist, s, c->gate);
             ++c->launches;
             c->vec(1, 3, P_D, P_D, P_Z, 0.0, beta);  // d = z + beta d (unused once converged)
-            settle(0);
+            c->gate = nullptr;
+            if (++in_batch == batch || k + 1 == cfg->max_iter) {
+                settle(0);
+                in_batch = 0;
+            }
         }
+        c->gate = nullptr;
         const int64_t its = c->h_ost->its;
         const bool conv = c->h_ost->converged != 0;
         // refresh: A u = f - B^T p, warm start from u (schur.py:352-357)

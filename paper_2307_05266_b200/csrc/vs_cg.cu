@@ -40,6 +40,18 @@ namespace vs {
 // unchanged, so U = 1 and U = 2 give bitwise the same results.
 template <int DIM, int OP, int TIER, bool QR = false, int U_ = 1>
 __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
+    if (P.gate && *P.gate) {  // enqueued ahead of the host, and the outer loop is already over
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            CgOut *o = P.out;
+            o->iterations = 0;
+            o->converged = 1;
+            o->status = 0;
+            o->value = 0.0;
+            o->at_iter = 0;
+            o->res_prec0 = o->res_unprec0 = o->res_prec_last = o->res_unprec_last = 0.0;
+        }
+        return;
+    }
     constexpr int U = U_ > 0 ? U_ : 1;  // U_ == 0: P1 with carried delta words (TIER 4)
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
@@ -468,6 +480,18 @@ __global__ void __launch_bounds__(CG_THREADS, 1) k_pcg(const CgParams P) {
 // 2 %, solutions within 1e-8); elementwise order is no longer bitwise.
 template <int DIM, int OP, int TIER, int NT>
 __global__ void __launch_bounds__(NT, 1) k_cg1(const CgParams P) {
+    if (P.gate && *P.gate) {  // enqueued ahead of the host, and the outer loop is already over
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            CgOut *o = P.out;
+            o->iterations = 0;
+            o->converged = 1;
+            o->status = 0;
+            o->value = 0.0;
+            o->at_iter = 0;
+            o->res_prec0 = o->res_unprec0 = o->res_prec_last = o->res_unprec_last = 0.0;
+        }
+        return;
+    }
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
     constexpr int KS = PROJ ? 6 : 3;  // per-iteration sums

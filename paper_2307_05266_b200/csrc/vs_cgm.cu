@@ -174,6 +174,18 @@ void launch_build_ctab(int op, const double2 *sdiag2, const double *diag_code, d
 // ---- the kernel -----------------------------------------------------------
 template <int DIM, int OP, bool RC, int NT>
 __global__ void __launch_bounds__(NT, 1) k_pcgm(const CgParams P) {
+    if (P.gate && *P.gate) {  // enqueued ahead of the host, and the outer loop is already over
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            CgOut *o = P.out;
+            o->iterations = 0;
+            o->converged = 1;
+            o->status = 0;
+            o->value = 0.0;
+            o->at_iter = 0;
+            o->res_prec0 = o->res_unprec0 = o->res_prec_last = o->res_unprec_last = 0.0;
+        }
+        return;
+    }
     constexpr bool PROJ = (OP == 1);
     constexpr int NS = 2 * DIM;
     __shared__ double s_tab[48];  // [40..47]: S_hat face weights times inv_h^2 (qrec form)

@@ -78,6 +78,7 @@ struct CgParams {
     const double2 *ctab;           // {1/diag, diag} by 2-B code index (k_pcgm)
     uint32_t cache_slots;
     uint32_t pf_dist;              // L2 prefetch distance in grid strides (0 = off)
+    const int *gate;               // outer-loop gate (OuterState.stop): != 0 -> this solve is a no-op
     unsigned long long *phase_ns;  // optional [12] accumulators
     uint32_t dbg;                  // VOXSCHUR_DBG bits (timing experiments only; results are wrong):
                                    // 1 = P1 gathers read the DOF's own value
@@ -101,20 +102,21 @@ void launch_slab_rec(const uint64_t *grec, uint64_t *lrec, int64_t count, int x_
 void launch_apply_A(const Geo &g, const uint64_t *rec, const double *u, double *out, int64_t m,
                     const double *diag_code, double inv_h2, cudaStream_t s);
 void launch_apply_div(const Geo &g, const uint64_t *prec, const double *u, double *out, int64_t m, double inv_h,
-                      cudaStream_t s);
+                      cudaStream_t s, const int *gate = nullptr);
 void launch_apply_grad(const Geo &g, const uint64_t *vrec, const double *p, double *out, int64_t m,
-                       double inv_h, cudaStream_t s);
+                       double inv_h, cudaStream_t s, const int *gate = nullptr);
 void launch_apply_S(const Geo &g, const uint64_t *prec, const double *p, double *out, int64_t m,
                     const double *invA_enc, double inv_h, cudaStream_t s);
 void launch_dwd(const Geo &g, const uint64_t *prec, const double *w, double *out, int64_t m, double inv_h2,
                 cudaStream_t s);
 void launch_vec(int kind, double *out, double *a, const double *b, double sc, const double *sp, int64_t m,
-                cudaStream_t s);
+                cudaStream_t s, const int *gate = nullptr);
 
 // device-side state of the outer PCG (vs_api.cu drives it, one sync per outer iteration)
 struct OuterState {
     double rz, alpha, beta, mu, ref, value;
     int32_t status, converged;  // status: 1 r'z < 0, 2 d'q <= 0, 3 non-finite
+    int32_t stop, _pad;         // converged or failed: the gate of kernels enqueued ahead of the host
     int64_t at, its, hstride;
 };
 enum { SO_MEAN, SO_PERM, SO_INIT, SO_ALPHA, SO_BETA };
@@ -122,10 +124,10 @@ enum { Q_DQ, Q_PERM, Q_MU, Q_RZ, Q_ZZ, Q_RR, Q_HOST, Q_COUNT };  // reduction sl
 void launch_xbar(unsigned *bar, unsigned *bar_base, int nranks, volatile int *xflag, unsigned long long timeout_ns,
                  cudaStream_t s);
 void launch_outer(int op, OuterState *st, const double *scal, int R, double arg, int64_t k, double eps,
-                  int use_prec, double *hist, cudaStream_t s);
+                  int use_prec, double *hist, cudaStream_t s, const int *gate = nullptr);
 void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s);
 int launch_reduce(int kind, const double *a, const double *b, int64_t m, double *part, double *out,
-                  cudaStream_t s);
+                  cudaStream_t s, const int *gate = nullptr);
 // connected components on the GPU (vs_cc.cu)
 constexpr int64_t CC_DEVICE_CELLS = (int64_t)1 << 22;  // assemble checks larger grids on the device
 size_t cc_work_bytes(int64_t N);

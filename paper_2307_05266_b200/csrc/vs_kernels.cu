@@ -183,9 +183,9 @@ __global__ void k_apply_A(Geo g, const uint64_t *rec, const double *u, double *o
 
 // B (operators.py:137-144): out = 0; out += u_in - u_out per axis; * inv_h
 __global__ void k_apply_div(Geo g, const uint64_t *prec, const double *u, double *out, int64_t m,
-                            double inv_h) {
+                            double inv_h, const int *gate) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= m) return;
+    if (i >= m || (gate && *gate)) return;
     const uint64_t r = prec[i];
     const Cell c = rec_cell(r);
     double acc = 0.0;
@@ -200,9 +200,9 @@ __global__ void k_apply_div(Geo g, const uint64_t *prec, const double *u, double
 
 // B^T (operators.py:146-153): (p[I] - p[I - e_a]) * inv_h
 __global__ void k_apply_grad(Geo g, const uint64_t *vrec, const double *p, double *out, int64_t m,
-                             double inv_h) {
+                             double inv_h, const int *gate) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= m) return;
+    if (i >= m || (gate && *gate)) return;
     const uint64_t r = vrec[i];
     const Cell c = rec_cell(r);
     const int a = rec_comp(r);
@@ -239,9 +239,13 @@ __global__ void k_dwd(Geo g, const uint64_t *prec, const double *w, double *out,
 
 // kind: 0 out=a-s ; 1 a-=s*b ; 2 a+=s*b ; 3 out=b+s*a (d = z + beta d) ; 4 out=a-b
 // s comes from the device scalar *sp when sp != nullptr (outer loop state)
-__global__ void k_vec(int kind, double *out, double *a, const double *b, double s0, const double *sp, int64_t m) {
+// gate (here and in the other outer-loop kernels): when the outer loop is enqueued several
+// iterations ahead of the host, *gate != 0 (converged or failed: OuterState.stop) turns
+// every later kernel into a no-op
+__global__ void k_vec(int kind, double *out, double *a, const double *b, double s0, const double *sp, int64_t m,
+                      const int *gate) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= m) return;
+    if (i >= m || (gate && *gate)) return;
     const double s = sp ? *sp : s0;
     switch (kind) {
         case 0: out[i] = __dsub_rn(a[i], s); break;
@@ -263,8 +267,9 @@ __global__ void k_force(double *out, const double *sub, int64_t lo, int64_t cnt,
 
 // deterministic two-stage reduction: kind 0 sum(a), 1 dot(a, b)
 __global__ void __launch_bounds__(RED_THREADS) k_reduce1(int kind, const double *a, const double *b,
-                                                         int64_t m, double *part) {
+                                                         int64_t m, double *part, const int *gate) {
     __shared__ double sw[RED_THREADS / 32];
+    if (gate && *gate) return;  // uniform over the grid
     double acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)RED_THREADS + threadIdx.x; i < m;
          i += (int64_t)gridDim.x * RED_THREADS)
@@ -279,7 +284,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce1(int kind, const double 
     }
 }
 
-__global__ void k_reduce2(const double *part, int nparts, double *out) {
+__global__ void k_reduce2(const double *part, int nparts, double *out, const int *gate) {
+    if (gate && *gate) return;
     double acc = 0.0;
     for (int j = threadIdx.x; j < nparts; j += 32) acc = __dadd_rn(acc, part[j]);
     for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(~0u, acc, o));
@@ -339,12 +345,12 @@ void launch_apply_A(const Geo &g, const uint64_t *rec, const double *u, double *
     if (m) k_apply_A<<<nblk(m), 256, 0, s>>>(g, rec, u, out, m, diag_code, inv_h2);
 }
 void launch_apply_div(const Geo &g, const uint64_t *prec, const double *u, double *out, int64_t m, double inv_h,
-                      cudaStream_t s) {
-    if (m) k_apply_div<<<nblk(m), 256, 0, s>>>(g, prec, u, out, m, inv_h);
+                      cudaStream_t s, const int *gate) {
+    if (m) k_apply_div<<<nblk(m), 256, 0, s>>>(g, prec, u, out, m, inv_h, gate);
 }
 void launch_apply_grad(const Geo &g, const uint64_t *vrec, const double *p, double *out, int64_t m,
-                       double inv_h, cudaStream_t s) {
-    if (m) k_apply_grad<<<nblk(m), 256, 0, s>>>(g, vrec, p, out, m, inv_h);
+                       double inv_h, cudaStream_t s, const int *gate) {
+    if (m) k_apply_grad<<<nblk(m), 256, 0, s>>>(g, vrec, p, out, m, inv_h, gate);
 }
 void launch_apply_S(const Geo &g, const uint64_t *prec, const double *p, double *out, int64_t m,
                     const double *invA_enc, double inv_h, cudaStream_t s) {
@@ -355,8 +361,8 @@ void launch_dwd(const Geo &g, const uint64_t *prec, const double *w, double *out
     if (m) k_dwd<<<nblk(m), 256, 0, s>>>(g, prec, w, out, m, inv_h2);
 }
 void launch_vec(int kind, double *out, double *a, const double *b, double sc, const double *sp, int64_t m,
-                cudaStream_t s) {
-    if (m) k_vec<<<nblk(m), 256, 0, s>>>(kind, out, a, b, sc, sp, m);
+                cudaStream_t s, const int *gate) {
+    if (m) k_vec<<<nblk(m), 256, 0, s>>>(kind, out, a, b, sc, sp, m, gate);
 }
 
 // ---- device-side scalar steps of the outer PCG (krylov.py:102-182, schur.py:288)
@@ -367,7 +373,8 @@ __device__ __forceinline__ double slab_sum(const double *scal, int q, int R) {
 }
 
 __global__ void k_outer(int op, OuterState *st, const double *scal, int R, double arg, int64_t k, double eps,
-                        int use_prec, double *hist) {
+                        int use_prec, double *hist, const int *gate) {
+    if (gate && *gate) return;
     // hist layout: [0] alpha, [1] beta, [2] res_prec, [3] res_unprec, [4] perm; stride HSTRIDE
     double *h_alpha = hist, *h_beta = hist + st->hstride, *h_rp = hist + 2 * st->hstride,
            *h_ru = hist + 3 * st->hstride, *h_perm = hist + 4 * st->hstride;
@@ -414,6 +421,7 @@ __global__ void k_outer(int op, OuterState *st, const double *scal, int R, doubl
             break;
         }
     }
+    st->stop = (st->converged || st->status) ? 1 : 0;
 }
 
 // cross-rank barrier for the outer loop: one arrival per rank on the
@@ -447,17 +455,17 @@ void launch_xbar(unsigned *bar, unsigned *bar_base, int nranks, volatile int *xf
 }
 
 void launch_outer(int op, OuterState *st, const double *scal, int R, double arg, int64_t k, double eps,
-                  int use_prec, double *hist, cudaStream_t s) {
-    k_outer<<<1, 1, 0, s>>>(op, st, scal, R, arg, k, eps, use_prec, hist);
+                  int use_prec, double *hist, cudaStream_t s, const int *gate) {
+    k_outer<<<1, 1, 0, s>>>(op, st, scal, R, arg, k, eps, use_prec, hist, gate);
 }
 void launch_force(double *out, const double *sub, int64_t lo, int64_t cnt, int64_t m, cudaStream_t s) {
     if (m) k_force<<<nblk(m), 256, 0, s>>>(out, sub, lo, cnt, m);
 }
 int launch_reduce(int kind, const double *a, const double *b, int64_t m, double *part, double *out,
-                  cudaStream_t s) {
+                  cudaStream_t s, const int *gate) {
     int nb = (int)std::min<int64_t>(RED_MAX_BLOCKS, std::max<int64_t>(1, (m + 4 * RED_THREADS - 1) / (4 * RED_THREADS)));
-    k_reduce1<<<nb, RED_THREADS, 0, s>>>(kind, a, b, m, part);
-    k_reduce2<<<1, 32, 0, s>>>(part, nb, out);
+    k_reduce1<<<nb, RED_THREADS, 0, s>>>(kind, a, b, m, part, gate);
+    k_reduce2<<<1, 32, 0, s>>>(part, nb, out, gate);
     return 2;
 }
 
