@@ -93,7 +93,7 @@ __global__ void k_desc_scan(const CgGroup G, int n, int nw, int2 *xb) {
 // pass 2: pack
 template <int DIM, int OP>
 __global__ void k_desc_pack(const CgGroup G, int n, int nw, const int2 *xb, uint64_t *desc, uint16_t *cidx,
-                            unsigned long long *n_escape) {
+                            unsigned long long *n_escape, int force_escape) {
     constexpr int NS = 2 * DIM;
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= G.m_own) return;
@@ -123,6 +123,7 @@ __global__ void k_desc_pack(const CgGroup G, int n, int nw, const int2 *xb, uint
     }
     if (nr[NS - 2] != ABSENT && nr[NS - 2] != i + 1) esc = true;
     if (nr[NS - 1] != ABSENT && nr[NS - 1] != i - 1) esc = true;
+    if (force_escape) esc = true;  // test hook: every DOF through the record + bitmask lookup
     if (esc) {
         ex0 = DX_ESC;
         atomicAdd(n_escape, 1ull);
@@ -159,12 +160,14 @@ void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const in
                       uint16_t *cidx, unsigned long long *n_escape, cudaStream_t s) {
     if (!G.m_own) return;
     const unsigned nb = (G.m_own + 255) / 256;
+    const char *ee = getenv("VOXSCHUR_DESC_ESCAPE");  // test hook: 1 = mark every DOF as an escape
+    const int fe = ee && atoi(ee) == 1;
     if (dim == 3)
-        op == 0 ? k_desc_pack<3, 0><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape)
-                : k_desc_pack<3, 1><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape);
+        op == 0 ? k_desc_pack<3, 0><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe)
+                : k_desc_pack<3, 1><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe);
     else
-        op == 0 ? k_desc_pack<2, 0><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape)
-                : k_desc_pack<2, 1><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape);
+        op == 0 ? k_desc_pack<2, 0><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe)
+                : k_desc_pack<2, 1><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe);
 }
 void launch_build_ctab(int op, const double2 *sdiag2, const double *diag_code, double2 *ctab, int count,
                        cudaStream_t s) {
