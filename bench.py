@@ -576,6 +576,43 @@ def run_ours(a):
                                 "achieved_gbs": BYTES_PER_DOF_ITER * v[0] / (v[1] / 1e3) / 1e9 if v[1] else 0.0}
                             for k, v in perk.items()}}
 
+    # extras (N = 1): the same fused kernels on the other 3D configs -- one inner
+    # A-solve and one inner S_hat-solve at C2 256^3 (us per CG iteration, fraction of
+    # the copy peak) and the C1 64^3 solves to tolerance.  Not part of the timed region.
+    extras = None
+    if world == 1 and not a.no_extras and a.config in ("C4", "C4L"):
+        extras = {}
+        del systems
+        g2 = configs.make_geometry("C2", a.seed, device=dev)
+        s2 = vx.assemble(g2, 0, device=dev)
+        pz = np.random.default_rng(1).standard_normal(s2.m_p)
+        pz -= pz.mean()
+        rhs = s2.apply_gradient(pz)
+        for _ in range(2):  # first = warm-up
+            vx.schur._solve_velocity(s2, rhs, 1e-12)
+            st_a = vx.last_kernel_stats(s2)["velocity_cg"]
+            vx.apply_simple_inverse(s2, pz, 1e-12)
+            st_s = vx.last_kernel_stats(s2)["simple_cg"]
+
+        def per_it(st):
+            ach = BYTES_PER_DOF_ITER * st["dof_iters"] / (st["ms"] / 1e3) / 1e9
+            return {"kernel": st["kernel"], "iterations": st["iterations"],
+                    "us_per_cg_iteration": 1e3 * st["ms"] / max(1, st["iterations"]), "achieved_gbs": ach,
+                    "frac": ach / peak}
+        extras["C2 256^3 spheres phi0.15 inner solves to 1e-12"] = {
+            "m_u": s2.m_u, "m_p": s2.m_p, "A": per_it(st_a), "S_hat": per_it(st_s)}
+        del s2
+        g1 = configs.make_geometry("C1", a.seed)
+        s1 = vx.assemble(g1, 0, device=dev)
+        c1 = {}
+        for prec in ("uzawa", "simple"):
+            for _ in range(2):
+                r1 = vx.solve_schur(s1, vx.SchurConfig(prec=prec, **TOL), return_fields=False)
+            c1[prec] = {"device_ms": r1.device_ms, "iters_outer": r1.iters_outer, "inner": r1.inner_iter_totals,
+                        "k": r1.k_value, "converged": r1.converged}
+        extras["C1 64^3 spheres phi0.4 solve_schur to tolerance"] = c1
+        del s1
+
     line = None
     if rank == 0:
         cpu = None
@@ -605,7 +642,7 @@ def run_ours(a):
             "setup_s": {"generate_mask": t_gen, "assemble": t_asm},
             "solves": last,
             "inner_iterations_per_step": {"A": tot["IA"] // a.steps, "S_hat": tot["IS"] // a.steps},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "extras": extras, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": tot["launches"], "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -627,6 +664,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end steps (long evidence runs)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C2 / C1 extra measurements")
     ap.add_argument("--sequential", action="store_true",
                     help="run the step's solves one after another on the whole device")
     ap.add_argument("--replicas", action="store_true",
