@@ -227,7 +227,9 @@ typedef struct {
                              iteration, reference operation order), 1 k_cg1
                              (one grid sum), 2 k_cg1t (one grid sum, tiled), 3 k_pcg
                              with q by recurrence, 4 / 5 k_pcgm (M-scaled over 8-B
-                             descriptors; s = M q by recurrence / q recomputed) */
+                             descriptors; s = M q by recurrence / q recomputed), 6 k_pcgb
+                             (experimental: S_hat on a blocked order with shared-memory
+                             windows) */
     int32_t reserved;
     int32_t tier;         /* where the fused CG took its neighbour ranks from:
                              1 bitmask lookups (records smem-cached), 2 ranks in

@@ -98,6 +98,12 @@ struct Slab {
     uint64_t *desc[2] = {nullptr, nullptr};
     uint16_t *cidx[2] = {nullptr, nullptr};
     int2 *xb[2] = {nullptr, nullptr};  // x+ / x- rank-distance bases per chunk of 1024 ranks
+    // k_pcgb (S_hat, blocked order): 0 = not built, 1 = built, -1 = not applicable here
+    int blk_state = 0;
+    uint32_t *blk_lineR = nullptr, *blk_lineI = nullptr, *blk_tile0 = nullptr, *blk_tl_src = nullptr;
+    uint16_t *blk_tl_len = nullptr, *blk_tl_v = nullptr, *blk_vidx = nullptr, *blk_cidx = nullptr;
+    uint64_t *blk_desc = nullptr;
+    int blk_ntiles = 0, blk_vcap = 0, blk_vbuf = 1;
     int64_t n_escape[2] = {0, 0};
     double *u[NU] = {}, *p[NP] = {};
     Geo geo{};
@@ -460,7 +466,7 @@ Status cg_status_to_error(const CgOut &o, int which) {
     return {VS_OK, ""};
 }
 
-inline bool is_m_alg(int alg) { return alg == CG_TWO_SUM_MQ || alg == CG_TWO_SUM_MRC; }
+inline bool is_m_alg(int alg) { return alg == CG_TWO_SUM_MQ || alg == CG_TWO_SUM_MRC || alg == CG_BLOCKED; }
 
 // k_pcgm descriptors of one slab and operator (vs_cgm.cu): the x-bases per
 // chunk of 1024 ranks, then the packed descriptors.  Runs once, on the first
@@ -491,6 +497,96 @@ void build_descriptors(vs_ctx *c, Slab &S, const CgGroup &G, int op) {
     }
 }
 
+// k_pcgb tables of the (single) slab's pressure family: line starts in both orders,
+// tiles, line slots and window offsets (host), then the per-DOF descriptors (device).
+// Leaves S.blk_state = -1 where the blocked kernel does not apply.
+void build_blocked(vs_ctx *c, Slab &S, const CgGroup &G) {
+    constexpr int TB = 8, TS = 10, NSLOT = 100;
+    const int n = c->n;
+    S.blk_state = -1;
+    if (c->dim != 3 || c->R != 1 || n % TB || n < 2 * TB || !S.m_own[1]) return;
+    const size_t nl = (size_t)n * n;
+    std::vector<uint32_t> R(nl + 1), I(nl);
+    // meta[(x*n + y) * nw].y = reference rank of the line's first DOF
+    CK(cudaMemcpy2DAsync(R.data(), sizeof(uint32_t), reinterpret_cast<const char *>(c->pmeta) + sizeof(uint32_t),
+                         (size_t)c->nw * sizeof(uint2), sizeof(uint32_t), nl, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    R[nl] = (uint32_t)S.m_own[1];
+    const int nt = n / TB, ntiles = nt * nt;
+    std::vector<uint32_t> tile0(ntiles + 1), tl_src((size_t)ntiles * NSLOT, 0);
+    std::vector<uint16_t> tl_len((size_t)ntiles * NSLOT, 0), tl_v((size_t)ntiles * NSLOT, 0);
+    uint32_t run = 0;
+    for (int X = 0; X < nt; ++X)
+        for (int Y = 0; Y < nt; ++Y) {
+            tile0[X * nt + Y] = run;
+            for (int px = 0; px < TB; ++px)
+                for (int py = 0; py < TB; ++py) {
+                    const size_t l = (size_t)(X * TB + px) * n + (Y * TB + py);
+                    I[l] = run;
+                    run += R[l + 1] - R[l];
+                }
+        }
+    tile0[ntiles] = run;
+    int vcap = 0;
+    for (int X = 0; X < nt; ++X)
+        for (int Y = 0; Y < nt; ++Y) {
+            const size_t t = (size_t)X * nt + Y;
+            uint32_t cur = 0;
+            for (int px = -1; px <= TB; ++px)
+                for (int py = -1; py <= TB; ++py) {
+                    if ((px < 0 || px == TB) && (py < 0 || py == TB)) continue;  // corners: no neighbour there
+                    const size_t l = (size_t)((X * TB + px + n) % n) * n + (size_t)((Y * TB + py + n) % n);
+                    const uint32_t L = R[l + 1] - R[l];
+                    const size_t k = t * NSLOT + (size_t)(px + 1) * TS + (py + 1);
+                    if (!L) continue;
+                    if (L > 500) return;  // y distances must fit 10 bits
+                    cur += 1;  // pad: the line's last DOF (periodic z wrap)
+                    tl_src[k] = I[l];
+                    tl_len[k] = (uint16_t)L;
+                    tl_v[k] = (uint16_t)cur;
+                    cur += L + 1;  // + pad: the line's first DOF
+                    if (cur > 60000) return;
+                }
+            vcap = std::max<int>(vcap, (int)cur + 2);
+        }
+    vcap = (vcap + 1) & ~1;  // windows 16-B aligned
+    const int vbuf = pcgb_fits(vcap, c->device);
+    if (!vbuf) return;
+    S.blk_vbuf = (getenv("VOXSCHUR_BLK_BUFS") && atoi(getenv("VOXSCHUR_BLK_BUFS")) == 1) ? 1 : vbuf;
+    auto up = [&](auto *&dst, const auto &v) {
+        using T = typename std::remove_reference<decltype(v[0])>::type;
+        dst = c->alloc<typename std::remove_const<T>::type>(v.size());
+        CK(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    };
+    up(S.blk_lineR, R);
+    up(S.blk_lineI, I);
+    up(S.blk_tile0, tile0);
+    up(S.blk_tl_src, tl_src);
+    up(S.blk_tl_len, tl_len);
+    up(S.blk_tl_v, tl_v);
+    const int64_t m = S.m_own[1];
+    S.blk_desc = c->alloc<uint64_t>(m);
+    S.blk_vidx = c->alloc<uint16_t>(m);
+    S.blk_cidx = c->alloc<uint16_t>(m);
+    int *bad = c->alloc<int>(1);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+    launch_blk_build(G, n, c->nw, S.blk_lineR, S.blk_lineI, S.blk_tl_v, S.blk_desc, S.blk_vidx, S.blk_cidx, bad,
+                     c->stream);
+    CK(cudaGetLastError());
+    int hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();  // the host tables must outlive their uploads
+    if (hbad) return;  // a window distance did not fit its field
+    if (!c->ctab[1]) {
+        c->ctab[1] = c->alloc<double2>(46656);
+        launch_build_ctab(1, c->sdiag2, c->d_diag_code, c->ctab[1], 46656, c->stream);
+        CK(cudaGetLastError());
+    }
+    S.blk_ntiles = ntiles;
+    S.blk_vcap = vcap;
+    S.blk_state = 1;
+}
+
 constexpr int GROUP_RING = 8;  // group-table staging slots (>= launches between syncs)
 
 // Launch one fused device PCG solve over all slabs (one cooperative launch)
@@ -509,6 +605,22 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         return li;
     }
     if (x0 >= 0) c->halo(op == 0 ? 0 : 1, x0);  // A x0 needs x0 on the ghost planes
+    // k_pcgb (S_hat on the blocked order): built on first use; where it does not apply
+    // (2D, slabs, n not a multiple of 8, ...) the solve takes k_pcgm
+    bool use_blocked = false;
+    if (op == 1 && c->plan_S.alg == CG_BLOCKED && x0 < 0 && !c->use_tile[1]) {
+        Slab &S0 = c->slabs[c->s0];
+        if (S0.blk_state == 0) {
+            CgGroup G0{};
+            memset(&G0, 0, sizeof G0);
+            G0.meta[0] = S0.meta[FP];
+            G0.rec = S0.prec;
+            G0.nx = S0.nx;
+            G0.m_own = (uint32_t)S0.m_own[1];
+            build_blocked(c, S0, G0);
+        }
+        use_blocked = S0.blk_state == 1;
+    }
     const int ring = li % GROUP_RING;
     const int nloc = c->s1 - c->s0;
     CgGroup *hg = c->h_groups + ring * nloc;
@@ -546,11 +658,28 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
             }
             G.nbr = nb;
         }
-        if (is_m_alg((op == 0 ? c->plan_A : c->plan_S).alg)) {
+        if (is_m_alg((op == 0 ? c->plan_A : c->plan_S).alg) && !use_blocked) {
             if (!S.desc[op]) build_descriptors(c, S, G, op);
             G.desc = S.desc[op];
             G.cidx = S.cidx[op];
             G.xb = S.xb[op];
+        }
+        if (use_blocked) {  // k_pcgb: the solve runs in the blocked order
+            G.desc = S.blk_desc;
+            G.cidx = S.blk_cidx;
+            G.vidx = S.blk_vidx;
+            G.tile0 = S.blk_tile0;
+            G.tl_src = S.blk_tl_src;
+            G.tl_len = S.blk_tl_len;
+            G.tl_v = S.blk_tl_v;
+            G.ntiles = S.blk_ntiles;
+            G.vcap = S.blk_vcap;
+            G.vbuf = S.blk_vbuf;
+            launch_blk_perm(S.prec, c->n, S.blk_lineR, S.blk_lineI, (uint32_t)S.m_own[1], v[rhs], S.p[P_SR], 1,
+                            c->stream);
+            ++c->launches;
+            G.rhs = S.p[P_SR];
+            G.x = S.p[P_SS0];
         }
         // k_cg1 buffers (the same slots, paired)
         G.zb[0] = G.z;
@@ -630,8 +759,17 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         P.total_blocks = tp.grid;
         P.block_base = 0;
         CK(launch_cg1t(op, tp, P, c->stream));
+    } else if (use_blocked) {
+        Slab &S0 = c->slabs[c->s0];
+        CK(launch_pcgb(pl, P, S0.blk_vcap, S0.blk_vbuf, c->stream));
+        // the solution back into the reference order
+        launch_blk_perm(S0.prec, c->n, S0.blk_lineR, S0.blk_lineI, (uint32_t)S0.m_own[1], S0.p[P_SS0], S0.p[x], 0,
+                        c->stream);
+        ++c->launches;
     } else if (is_m_alg(pl.alg)) {
-        CK(launch_pcgm(c->dim, op, pl, nloc, P, c->stream));
+        CgPlan pm = pl;
+        if (pm.alg == CG_BLOCKED) pm.alg = CG_TWO_SUM_MQ;  // k_pcgb does not apply here
+        CK(launch_pcgm(c->dim, op, pm, nloc, P, c->stream));
     } else {
         CK(launch_pcg(c->dim, op, pl, nloc, P, c->stream));
     }
@@ -657,6 +795,7 @@ void drain_log(vs_ctx *c, int from, int64_t *its_op) {
         st.dof_iters += o.iterations * m;
         st.ms += ms;
         st.kernel = c->use_tile[op] ? 2 : (op == 0 ? c->plan_A.alg : c->plan_S.alg);
+        if (st.kernel == CG_BLOCKED && c->slabs[c->s0].blk_state != 1) st.kernel = CG_TWO_SUM_MQ;
         st.reserved = op == 0 ? c->plan_A.unroll : c->plan_S.unroll;  // P1 DOFs per step
         st.tier = op == 0 ? c->plan_A.tier : c->plan_S.tier;
         {
@@ -943,6 +1082,7 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     // VOXSCHUR_CG forces a kernel: 1 k_cg1, 2 k_pcg (reference operation order),
     // 3 k_pcg<QR>, 4 k_pcgm qrec, 5 k_pcgm rc (q recomputed in both passes, 80 B).
     auto pick = [&](int64_t m, int op) {
+        if (force == 6) return op == 1 ? (int)CG_BLOCKED : (int)CG_TWO_SUM_MQ;
         if (force == 4) return (int)CG_TWO_SUM_MQ;
         if (force == 5) return (int)CG_TWO_SUM_MRC;
         if (force == 3) return (int)CG_TWO_SUM_QREC;

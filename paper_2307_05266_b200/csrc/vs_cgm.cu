@@ -590,7 +590,7 @@ CgPlan pcgm_plan(int dim, int op, int64_t m, int groups, int device, int alg, in
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     if (sms > 0 && sms < nsm) nsm = sms;
-    const void *fn = pcgm_fn(dim, op, alg == CG_TWO_SUM_MRC, nt);
+    const void *fn = pcgm_fn(dim, op, alg == CG_TWO_SUM_MRC, nt);  // CG_BLOCKED plans like the qrec form
     pl.smem = 0;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, pl.smem);

@@ -40,6 +40,12 @@ struct CgGroup {
     const uint64_t *desc;
     const uint16_t *cidx;
     const int2 *xb;
+    // k_pcgb (vs_cgb.cu): blocked order -- tile starts [ntiles + 1], per tile and line slot
+    // the line's first blocked rank, its DOFs and its offset in the shared-memory window;
+    // per DOF its index in the window; window capacity in doubles
+    const uint32_t *tile0, *tl_src;
+    const uint16_t *tl_len, *tl_v, *vidx;
+    int ntiles, vcap, vbuf;
     const uint32_t *nbr;            // TIER 3: neighbour ranks [2*dim][m_own] (ABSENT if none);
                                     // TIER 4: int2 x-deltas [m_own], then short2 y-deltas [m_own] (3D)
     // halo: side s = 0 sends the first owned plane to the lower neighbour's
@@ -138,7 +144,10 @@ constexpr size_t CG_SMEM_BUDGET = 200 * 1024;  // dynamic smem per block (1 bloc
 // (value 3: 2 is the k_cg1t kernel id in vs_kstat)
 // 4, 5: k_pcgm (vs_cgm.cu), M-scaled over 8-B descriptors: s = M q by
 // recurrence / q = A d recomputed in both passes
-enum CgAlg { CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3, CG_TWO_SUM_MQ = 4, CG_TWO_SUM_MRC = 5 };
+// 6: k_pcgb (vs_cgb.cu), the qrec form on the blocked order with shared-memory windows (S_hat, 3D, one slab)
+enum CgAlg {
+    CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3, CG_TWO_SUM_MQ = 4, CG_TWO_SUM_MRC = 5, CG_BLOCKED = 6
+};
 struct CgPlan {
     int alg;
     int unroll;   // DOFs per P1 step (k_pcg<QR> only)
@@ -159,6 +168,14 @@ cudaError_t launch_pcgm(int dim, int op, const CgPlan &pl, int groups, CgParams 
 void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, int2 *xb, cudaStream_t s);
 void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int2 *xb, uint64_t *desc,
                       uint16_t *cidx, unsigned long long *n_escape, cudaStream_t s);
+// k_pcgb (vs_cgb.cu)
+void launch_blk_build(const CgGroup &G, int n, int nw, const uint32_t *lineR, const uint32_t *lineI,
+                      const uint16_t *tl_v, uint64_t *desc, uint16_t *vidx, uint16_t *cidx, int *bad, cudaStream_t s);
+void launch_blk_perm(const uint64_t *rec, int n, const uint32_t *lineR, const uint32_t *lineI, uint32_t m,
+                     const double *in, double *out, int to_blocked, cudaStream_t s);
+size_t pcgb_smem(int vcap, int nbuf);
+int pcgb_fits(int vcap, int device);
+cudaError_t launch_pcgb(const CgPlan &pl, CgParams &P, int vcap, int nbuf, cudaStream_t s);
 void launch_build_ctab(int op, const double2 *sdiag2, const double *diag_code, double2 *ctab, int count,
                        cudaStream_t s);
 

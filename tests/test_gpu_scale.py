@@ -149,3 +149,25 @@ def test_c2_properties(c2):
     x, its = schur._solve_velocity(s, rhs, 1e-12)
     res = s.apply_laplacian(x) - rhs
     assert np.linalg.norm(res) <= 1e-9 * np.linalg.norm(rhs)
+
+
+def test_c1_blocked_kernel_vs_oracle(c1, monkeypatch):
+    """k_pcgb: the S_hat solve on the blocked DOF order with the neighbour values
+    staged in shared memory (VOXSCHUR_CG=6), against the oracle at C1 64^3."""
+    grid, _, o = c1
+    monkeypatch.setenv("VOXSCHUR_CG", "6")
+    s = vx.assemble(grid, 0)
+    rng = np.random.default_rng(5)
+    p = rng.standard_normal(s.m_p)
+    p -= p.mean()
+    z = vx.apply_simple_inverse(s, p, 1e-12)
+    zo, io = vo.solve_simple(o, p, 1e-12)
+    st = vx.last_kernel_stats(s)["simple_cg"]
+    assert st["kernel"] == "k_pcgb" and within_2pct(st["iterations"], io)
+    assert rel_err(z, zo) < REL
+    # a full SIMPLE solve through it, capped, against the oracle
+    kw = dict(eps_S=1e-8, eps_A=1e-12, eps_Shat=1e-12, max_iter=2)
+    rep = vx.solve_schur(s, vx.SchurConfig(prec="simple", **kw))
+    orc = vo.solve_schur(o, "simple", **kw)
+    assert rel_err(rep.pressure, orc["pressure"]) < REL and rel_err(rep.velocity, orc["velocity"]) < REL
+    assert within_2pct(rep.inner_iter_totals["preconditioner"], orc["inner_iter_totals"]["preconditioner"])
