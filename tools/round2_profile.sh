@@ -10,7 +10,7 @@ fi
 timeout 1500 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err; cat gpurun_out/${tag}_bench.json | cut -c1-3000
 tail -3 gpurun_out/${tag}_bench.err
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 40000 --csv \
-  --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu \
+  --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-extras \
   > gpurun_out/${tag}_ncu_list.log 2>&1
 python tools/launch_share.py gpurun_out/${tag}_launches.csv > gpurun_out/${tag}_launch_list.txt 2>&1; head -30 gpurun_out/${tag}_launch_list.txt
 VOXSCHUR_INNER_MAXIT=60 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_pcg" -c 2 \
