@@ -2,17 +2,21 @@
 // on a BLOCKED internal DOF order with the neighbour values staged in shared
 // memory.
 //
-// Why.  In the reference's packed order a DOF's x+- neighbours lie a whole
-// plane away, so P1's gathers come from L2, and on the B200 an L2 access costs
-// what a DRAM byte costs (both passes run at ~7 TB/s of
-// total L2 traffic; P1 moves 48 compulsory bytes plus ~24 B of gathers).  Here
+// Why it was built.  In the reference's packed order a DOF's x+- neighbours lie a
+// whole plane away, so P1's gathers come from L2; a reading of the k_pcgm
+// measurements suggested that those gathers cost as much as DRAM bytes.  Here
 // the pressure DOFs are stored tile by tile -- a tile is TB x TB lines (x, y)
 // with all their z -- and P1 works through one tile at a time: the tile's z
 // values and the one-plane / one-line halos around it are copied into shared
 // memory (each line padded with its own two ends, so that the periodic z wrap
 // is index +-1 too), and all six neighbours of a DOF are shared-memory reads
-// at tile-local distances held in the same 8-byte descriptor.  z then comes up
-// from L2 ~1.7x (tile + halo) instead of 1x + 3 gathered copies.
+// at tile-local distances held in the same 8-byte descriptor.
+//
+// What it showed.  Parity-green and 28 % slower than k_pcgm (B200, C4 512^3:
+// 615 vs 482 us/it).  A later timing experiment (all gathers of k_pcgm redirected
+// to the DOF's own index) put the whole cost of the gathers at 19 us of P1's
+// 248: there was never more than 4 % to win here.  Kept as
+// an opt-in experiment (VOXSCHUR_CG=6).
 //
 // Scope: S_hat (projected), 3D, one slab, n a multiple of TB; everything else
 // keeps k_pcgm.  The vectors live in the blocked order for the length of one
