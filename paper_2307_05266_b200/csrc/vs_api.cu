@@ -466,7 +466,9 @@ Status cg_status_to_error(const CgOut &o, int which) {
     return {VS_OK, ""};
 }
 
-inline bool is_m_alg(int alg) { return alg == CG_TWO_SUM_MQ || alg == CG_TWO_SUM_MRC || alg == CG_BLOCKED; }
+inline bool is_m_alg(int alg) {
+    return alg == CG_TWO_SUM_MQ || alg == CG_TWO_SUM_MRC || alg == CG_BLOCKED || alg == CG_TWO_SUM_MX;
+}
 
 // k_pcgm descriptors of one slab and operator (vs_cgm.cu): the x-bases per
 // chunk of 1024 ranks, then the packed descriptors.  Runs once, on the first
@@ -478,8 +480,8 @@ void build_descriptors(vs_ctx *c, Slab &S, const CgGroup &G, int op) {
     CK(cudaMemsetAsync(xb, 0x7F, (size_t)nchunk * sizeof(int2), c->stream));  // 0x7F7F7F7F: "no such neighbour here"
     launch_desc_scan(c->dim, op, G, c->n, c->nw, xb, c->stream);
     CK(cudaGetLastError());
-    S.desc[op] = c->alloc<uint64_t>(m);
-    S.cidx[op] = c->alloc<uint16_t>(m);
+    S.desc[op] = c->alloc<uint64_t>(m + 16);  // k_pcgx's bulk copies round a chunk's size up to 16 B
+    S.cidx[op] = c->alloc<uint16_t>(m + 16);
     unsigned long long *cnt = c->alloc<unsigned long long>(1);
     CK(cudaMemsetAsync(cnt, 0, sizeof *cnt, c->stream));
     launch_desc_pack(c->dim, op, G, c->n, c->nw, xb, S.desc[op], S.cidx[op], cnt, c->stream);
@@ -688,10 +690,17 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
         G.ub[1] = G.q;
         G.sb[0] = op == 0 ? S.u[U_S0] : S.p[P_SS0];
         G.sb[1] = op == 0 ? S.u[U_S1] : S.p[P_SS1];
+        // k_pcgx: the z ring (d = d0, s = q as in k_pcgm)
+        static const int ring_u[4] = {U_Z, U_R, U_D1, U_S0}, ring_p[4] = {P_SZ, P_SR, P_SD1, P_SS0};
+        for (int b = 0; b < 4; ++b) G.zr[b] = op == 0 ? S.u[ring_u[b]] : S.p[ring_p[b]];
         if (R > 1) {
             Slab &lo = c->slabs[(s - 1 + R) % R], &hi = c->slabs[(s + 1) % R];
             G.zpeer[0] = op == 0 ? lo.u[U_Z] : lo.p[P_SZ];
             G.zpeer[1] = op == 0 ? hi.u[U_Z] : hi.p[P_SZ];
+            for (int b = 0; b < 4; ++b) {
+                G.zrp[0][b] = op == 0 ? lo.u[ring_u[b]] : lo.p[ring_p[b]];
+                G.zrp[1][b] = op == 0 ? hi.u[ring_u[b]] : hi.p[ring_p[b]];
+            }
             const int nf = op == 0 ? c->dim : 1;
             for (int k = 0; k < nf; ++k) {
                 const int f = op == 0 ? k : FP;
@@ -769,7 +778,10 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     } else if (is_m_alg(pl.alg)) {
         CgPlan pm = pl;
         if (pm.alg == CG_BLOCKED) pm.alg = CG_TWO_SUM_MQ;  // k_pcgb does not apply here
-        CK(launch_pcgm(c->dim, op, pm, nloc, P, c->stream));
+        if (pm.alg == CG_TWO_SUM_MX)
+            CK(launch_pcgx(c->dim, op, pm, nloc, P, c->stream));
+        else
+            CK(launch_pcgm(c->dim, op, pm, nloc, P, c->stream));
     } else {
         CK(launch_pcg(c->dim, op, pl, nloc, P, c->stream));
     }
@@ -1083,6 +1095,7 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     // 3 k_pcg<QR>, 4 k_pcgm qrec, 5 k_pcgm rc (q recomputed in both passes, 80 B).
     auto pick = [&](int64_t m, int op) {
         if (force == 6) return op == 1 ? (int)CG_BLOCKED : (int)CG_TWO_SUM_MQ;
+        if (force == 7) return (int)CG_TWO_SUM_MX;
         if (force == 4) return (int)CG_TWO_SUM_MQ;
         if (force == 5) return (int)CG_TWO_SUM_MRC;
         if (force == 3) return (int)CG_TWO_SUM_QREC;
@@ -1112,6 +1125,7 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
                 const CgPlan q = pcg_plan(dim, op, m, nloc, C->device, CG_TWO_SUM_QREC, 0, nsm);
                 if (q.tier == 2) return q;
             }
+            if (alg == CG_TWO_SUM_MX) return pcgx_plan(dim, op, m, nloc, C->device, nsm);
             return pcgm_plan(dim, op, m, nloc, C->device, alg, nsm);
         }
         return pcg_plan(dim, op, m, nloc, C->device, alg, nbr_tier, nsm);

@@ -35,6 +35,10 @@ struct CgGroup {
     const double *rhs, *x0;
     double *x, *r, *z, *d0, *d1, *q;
     double *zb[2], *ub[2], *sb[2];  // k_cg1: double-buffered zr = M r, u = M A zr, s = M q
+    // k_pcgx (vs_cgx.cu): the ring of z buffers (iteration k lives in zr[k mod M]) and, per
+    // halo side, the neighbour slab's buffers (ghost planes)
+    double *zr[4];
+    double *zrp[2][4];
     // k_pcgm (vs_cgm.cu): 8-B descriptors, 2-B code indices and the x+ / x-
     // rank-distance bases per chunk of 1024 ranks
     const uint64_t *desc;
@@ -145,9 +149,14 @@ constexpr size_t CG_SMEM_BUDGET = 200 * 1024;  // dynamic smem per block (1 bloc
 // 4, 5: k_pcgm (vs_cgm.cu), M-scaled over 8-B descriptors: s = M q by
 // recurrence / q = A d recomputed in both passes
 // 6: k_pcgb (vs_cgb.cu), the qrec form on the blocked order with shared-memory windows (S_hat, 3D, one slab)
+// 7: k_pcgx (vs_cgx.cu): alpha from the z sums (no d in the stencil pass), z in a ring of
+//    M buffers, d and x brought up to date every M-th iteration: 90 / 78 / 74 / 72 B per
+//    DOF-iteration for M = 1..4
 enum CgAlg {
-    CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3, CG_TWO_SUM_MQ = 4, CG_TWO_SUM_MRC = 5, CG_BLOCKED = 6
+    CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3, CG_TWO_SUM_MQ = 4, CG_TWO_SUM_MRC = 5, CG_BLOCKED = 6,
+    CG_TWO_SUM_MX = 7
 };
+constexpr int PCGX_MAX_DEPTH = 4, PCGX_DEPTH_DEFAULT = 2;
 struct CgPlan {
     int alg;
     int unroll;   // DOFs per P1 step (k_pcg<QR> only)
@@ -168,6 +177,9 @@ cudaError_t launch_pcgm(int dim, int op, const CgPlan &pl, int groups, CgParams 
 void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, int2 *xb, cudaStream_t s);
 void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int2 *xb, uint64_t *desc,
                       uint16_t *cidx, unsigned long long *n_escape, cudaStream_t s);
+// k_pcgx (vs_cgx.cu); the plan's `unroll` carries the ring depth M
+CgPlan pcgx_plan(int dim, int op, int64_t m, int groups, int device, int sms = 0);
+cudaError_t launch_pcgx(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
 // k_pcgb (vs_cgb.cu)
 void launch_blk_build(const CgGroup &G, int n, int nw, const uint32_t *lineR, const uint32_t *lineI,
                       const uint16_t *tl_v, uint64_t *desc, uint16_t *vidx, uint16_t *cidx, int *bad, cudaStream_t s);

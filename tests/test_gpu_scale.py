@@ -79,7 +79,9 @@ def test_c1_capped_solve_vs_oracle(c1, prec):
 
 @pytest.mark.parametrize("env", [{"VOXSCHUR_CG": "2"}, {"VOXSCHUR_CG": "3"}, {"VOXSCHUR_CG": "4"},
                                  {"VOXSCHUR_CG": "5"}, {"VOXSCHUR_CG": "4", "VOXSCHUR_M_THREADS": "512"},
-                                 {"VOXSCHUR_CG": "5", "VOXSCHUR_M_THREADS": "512"}, {"VOXSCHUR_TILED": "1"}])
+                                 {"VOXSCHUR_CG": "5", "VOXSCHUR_M_THREADS": "512"}, {"VOXSCHUR_TILED": "1"},
+                                 {"VOXSCHUR_CG": "7", "VOXSCHUR_X_DEPTH": "1"}, {"VOXSCHUR_CG": "7", "VOXSCHUR_X_DEPTH": "2"},
+                                 {"VOXSCHUR_CG": "7", "VOXSCHUR_X_DEPTH": "3"}, {"VOXSCHUR_CG": "7", "VOXSCHUR_X_DEPTH": "4"}])
 def test_c1_other_kernels_vs_oracle(c1, monkeypatch, env):
     """The C1 inner solves with the two-reduction k_pcg (forced) and with the
     experimental TMA-staged plane sweep k_cg1t, against the oracle."""
@@ -87,7 +89,7 @@ def test_c1_other_kernels_vs_oracle(c1, monkeypatch, env):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     s = vx.assemble(grid, 0)
-    want = {"2": "k_pcg", "3": "k_pcg_qrec", "4": "k_pcgm_qrec", "5": "k_pcgm_rc"}[env["VOXSCHUR_CG"]] if "VOXSCHUR_CG" in env else "k_cg1t"
+    want = {"2": "k_pcg", "3": "k_pcg_qrec", "4": "k_pcgm_qrec", "5": "k_pcgm_rc", "7": "k_pcgx"}[env["VOXSCHUR_CG"]] if "VOXSCHUR_CG" in env else "k_cg1t"
     rng = np.random.default_rng(5)
     p = rng.standard_normal(s.m_p)
     p -= p.mean()
