@@ -98,6 +98,7 @@ struct Slab {
     uint64_t *desc[2] = {nullptr, nullptr};
     uint16_t *cidx[2] = {nullptr, nullptr};
     int2 *xb[2] = {nullptr, nullptr};  // x+ / x- rank-distance bases per chunk of 1024 ranks
+    uint32_t *esc[2] = {nullptr, nullptr};  // escape table: the gather indices of the DOFs outside the descriptor format
     // k_pcgb (S_hat, blocked order): 0 = not built, 1 = built, -1 = not applicable here
     int blk_state = 0;
     uint32_t *blk_lineR = nullptr, *blk_lineI = nullptr, *blk_tile0 = nullptr, *blk_tl_src = nullptr;
@@ -484,7 +485,13 @@ void build_descriptors(vs_ctx *c, Slab &S, const CgGroup &G, int op) {
     S.cidx[op] = c->alloc<uint16_t>(m + 16);
     unsigned long long *cnt = c->alloc<unsigned long long>(1);
     CK(cudaMemsetAsync(cnt, 0, sizeof *cnt, c->stream));
-    launch_desc_pack(c->dim, op, G, c->n, c->nw, xb, S.desc[op], S.cidx[op], cnt, c->stream);
+    // escape table: room for 1/16 of the DOFs (C4 512^3: 0.6 % escape; every DOF under the test
+    // hook VOXSCHUR_DESC_ESCAPE, where the slots run out and the rest take the record path)
+    uint32_t esc_cap = (uint32_t)std::min<int64_t>(m / 16 + 4096, (int64_t)1 << 30);
+    if (const char *e = getenv("VOXSCHUR_ESC_CAP"))  // test hook: a small table, so that both escape paths run
+        if (atoll(e) >= 0) esc_cap = (uint32_t)std::min<int64_t>(atoll(e), esc_cap);
+    S.esc[op] = c->alloc<uint32_t>((size_t)8 * esc_cap + 8);
+    launch_desc_pack(c->dim, op, G, c->n, c->nw, xb, S.desc[op], S.cidx[op], cnt, S.esc[op], esc_cap, c->stream);
     CK(cudaGetLastError());
     unsigned long long h = 0;
     CK(cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, c->stream));
@@ -665,6 +672,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
             G.desc = S.desc[op];
             G.cidx = S.cidx[op];
             G.xb = S.xb[op];
+            G.esc = reinterpret_cast<const uint4 *>(S.esc[op]);
         }
         if (use_blocked) {  // k_pcgb: the solve runs in the blocked order
             G.desc = S.blk_desc;
@@ -1086,13 +1094,14 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, C->device));
     if (sms > 0 && sms < nsm) nsm = sms;
     // Small operators (at most 4 DOFs per thread): k_cg1, one grid sum per
-    // iteration.  Everything larger, and every slab-decomposed run: k_pcgm in its
-    // qrec form (vs_cgm.cu: two grid sums, M-scaled, 8-B descriptors, 98 B per
-    // DOF-iteration).  B200, us per CG iteration, against the previous default
-    // k_pcg<QR> with packed deltas (124 B): C4 512^3 S_hat 637 -> 510, A 1392 ->
-    // 1113; C2 256^3 S_hat 53.0 -> 50.8, A 96.0 -> 87.3 (profiles/r02f_*, r02g_*).
-    // VOXSCHUR_CG forces a kernel: 1 k_cg1, 2 k_pcg (reference operation order),
-    // 3 k_pcg<QR>, 4 k_pcgm qrec, 5 k_pcgm rc (q recomputed in both passes, 80 B).
+    // iteration.  Everything larger, and every slab-decomposed run: k_pcgx (vs_cgx.cu:
+    // two grid sums, M-scaled, 8-B descriptors, alpha from the z sums, d and x brought
+    // up to date every 4th iteration from a ring of z buffers: 72 B per DOF-iteration).
+    // B200, us per CG iteration, against the previous default k_pcgm qrec (98 B):
+    // C4 512^3 S_hat 463 -> 403, A 1149 -> 822; C2 256^3 S_hat 47.3 -> 42.6, A 86.8 -> 79.0
+    // (profiles/r02x_*).  VOXSCHUR_CG forces a kernel: 1 k_cg1, 2 k_pcg (reference
+    // operation order), 3 k_pcg<QR>, 4 k_pcgm qrec, 5 k_pcgm rc (q recomputed in both
+    // passes, 80 B), 6 k_pcgb, 7 k_pcgx.
     auto pick = [&](int64_t m, int op) {
         if (force == 6) return op == 1 ? (int)CG_BLOCKED : (int)CG_TWO_SUM_MQ;
         if (force == 7) return (int)CG_TWO_SUM_MX;
@@ -1102,7 +1111,7 @@ void plan_solvers(vs_ctx *C, int64_t mu_max, int64_t mp_max, int sms) {
         if (force == 2) return (int)CG_TWO_SUM;
         if (R == 1 && (force == 1 || (force == 0 && m <= (int64_t)4 * nsm * CG_THREADS)))
             return (int)CG_ONE_SUM;
-        return (int)CG_TWO_SUM_MQ;
+        return (int)CG_TWO_SUM_MX;
     };
     const char *en = getenv("VOXSCHUR_NBR");
     // VOXSCHUR_NBR=1: TIER 3 (32-bit ranks), =2: TIER 4 (packed deltas)

@@ -62,7 +62,7 @@ __global__ void k_desc_scan(const CgGroup G, int n, int nw, int2 *xb) {
 // pass 2: pack
 template <int DIM, int OP>
 __global__ void k_desc_pack(const CgGroup G, int n, int nw, const int2 *xb, uint64_t *desc, uint16_t *cidx,
-                            unsigned long long *n_escape, int force_escape) {
+                            unsigned long long *n_escape, int force_escape, uint32_t *esc_tab, uint32_t esc_cap) {
     constexpr int NS = 2 * DIM;
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= G.m_own) return;
@@ -95,7 +95,14 @@ __global__ void k_desc_pack(const CgGroup G, int n, int nw, const int2 *xb, uint
     if (force_escape) esc = true;  // test hook: every DOF through the record + bitmask lookup
     if (esc) {
         ex0 = DX_ESC;
-        atomicAdd(n_escape, 1ull);
+        const unsigned long long e = atomicAdd(n_escape, 1ull);
+        ex1 = dy0 = dy1 = 0;
+        if (esc_tab && e < esc_cap) {  // the gather indices, for k_pcgx (slot order is arbitrary, the content is not)
+            uint32_t *t = esc_tab + 8 * e;
+#pragma unroll
+            for (int s = 0; s < 8; ++s) t[s] = (s < NS && nr[s] != ABSENT) ? nr[s] : i;
+            ex1 = e + 1;  // bits SH_EORD.. (33 bits)
+        }
     }
     desc[i] = rec_codes<OP>(rc) | (ex0 << SH_XP) | (ex1 << SH_XM) | (dy0 << SH_YP) | (dy1 << SH_YM);
     cidx[i] = (uint16_t)rec_cidx<DIM, OP>(rc);
@@ -126,17 +133,18 @@ void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, int2 *xb
         op == 0 ? k_desc_scan<2, 0><<<nb, 256, 0, s>>>(G, n, nw, xb) : k_desc_scan<2, 1><<<nb, 256, 0, s>>>(G, n, nw, xb);
 }
 void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int2 *xb, uint64_t *desc,
-                      uint16_t *cidx, unsigned long long *n_escape, cudaStream_t s) {
+                      uint16_t *cidx, unsigned long long *n_escape, uint32_t *esc_tab, uint32_t esc_cap,
+                      cudaStream_t s) {
     if (!G.m_own) return;
     const unsigned nb = (G.m_own + 255) / 256;
     const char *ee = getenv("VOXSCHUR_DESC_ESCAPE");  // test hook: 1 = mark every DOF as an escape
     const int fe = ee && atoi(ee) == 1;
     if (dim == 3)
-        op == 0 ? k_desc_pack<3, 0><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe)
-                : k_desc_pack<3, 1><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe);
+        op == 0 ? k_desc_pack<3, 0><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe, esc_tab, esc_cap)
+                : k_desc_pack<3, 1><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe, esc_tab, esc_cap);
     else
-        op == 0 ? k_desc_pack<2, 0><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe)
-                : k_desc_pack<2, 1><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe);
+        op == 0 ? k_desc_pack<2, 0><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe, esc_tab, esc_cap)
+                : k_desc_pack<2, 1><<<nb, 256, 0, s>>>(G, n, nw, xb, desc, cidx, n_escape, fe, esc_tab, esc_cap);
 }
 void launch_build_ctab(int op, const double2 *sdiag2, const double *diag_code, double2 *ctab, int count,
                        cudaStream_t s) {

@@ -37,6 +37,11 @@ __device__ __forceinline__ uint32_t rec_cidx(uint64_t rc) {
     for (int a = 2; a >= 0; --a) v = v * 6 + (uint32_t)rec_pin(rc, a);
     return v;
 }
+// An escape descriptor (x+ field = DX_ESC) keeps its 18 code bits; the 33 bits from SH_XM up hold
+// 1 + the DOF's slot in the escape table (8 x uint32 per slot: its 2*DIM gather indices, an
+// absent neighbour's = the DOF itself), or 0 when the table was full -- k_pcgx reads the slot
+// instead of the record + bitmask words (k_pcgm ignores the field).
+constexpr int SH_EORD = SH_XM;
 constexpr int CHUNK_SHIFT = 10;  // x-bases are kept per chunk of 1024 consecutive ranks
 
 }  // namespace vs

@@ -44,6 +44,7 @@ struct CgGroup {
     const uint64_t *desc;
     const uint16_t *cidx;
     const int2 *xb;
+    const uint4 *esc;  // escape table (vs_desc.cuh): two uint4 per slot
     // k_pcgb (vs_cgb.cu): blocked order -- tile starts [ntiles + 1], per tile and line slot
     // the line's first blocked rank, its DOFs and its offset in the shared-memory window;
     // per DOF its index in the window; window capacity in doubles
@@ -156,7 +157,7 @@ enum CgAlg {
     CG_TWO_SUM = 0, CG_ONE_SUM = 1, CG_TWO_SUM_QREC = 3, CG_TWO_SUM_MQ = 4, CG_TWO_SUM_MRC = 5, CG_BLOCKED = 6,
     CG_TWO_SUM_MX = 7
 };
-constexpr int PCGX_MAX_DEPTH = 4, PCGX_DEPTH_DEFAULT = 2;
+constexpr int PCGX_MAX_DEPTH = 4, PCGX_DEPTH_DEFAULT = 4;
 struct CgPlan {
     int alg;
     int unroll;   // DOFs per P1 step (k_pcg<QR> only)
@@ -176,7 +177,8 @@ CgPlan pcgm_plan(int dim, int op, int64_t m, int groups, int device, int alg, in
 cudaError_t launch_pcgm(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
 void launch_desc_scan(int dim, int op, const CgGroup &G, int n, int nw, int2 *xb, cudaStream_t s);
 void launch_desc_pack(int dim, int op, const CgGroup &G, int n, int nw, const int2 *xb, uint64_t *desc,
-                      uint16_t *cidx, unsigned long long *n_escape, cudaStream_t s);
+                      uint16_t *cidx, unsigned long long *n_escape, uint32_t *esc_tab, uint32_t esc_cap,
+                      cudaStream_t s);
 // k_pcgx (vs_cgx.cu); the plan's `unroll` carries the ring depth M
 CgPlan pcgx_plan(int dim, int op, int64_t m, int groups, int device, int sms = 0);
 cudaError_t launch_pcgx(int dim, int op, const CgPlan &pl, int groups, CgParams &P, cudaStream_t s);
