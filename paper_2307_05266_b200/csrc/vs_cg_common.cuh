@@ -307,7 +307,7 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
     if (warp < K) {
         // chunks of 8 (pairwise within a chunk), then the chunk sums pairwise
         constexpr int NC = NT / 256;
-        static_assert(NC == 2 || NC == 4, "grid_sum block stage: 512 or 1024 threads");
+        static_assert(NC == 2 || NC == 3 || NC == 4, "grid_sum block stage: 512, 768 or 1024 threads");
         double c[NC];
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
@@ -324,6 +324,8 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
         double t[1];
         if constexpr (NC == 4)
             t[0] = __dadd_rn(__dadd_rn(c[0], c[1]), __dadd_rn(c[2], c[3]));
+        else if constexpr (NC == 3)
+            t[0] = __dadd_rn(__dadd_rn(c[0], c[1]), c[2]);
         else
             t[0] = __dadd_rn(c[0], c[1]);
         warp_tree<1>(t);

@@ -53,6 +53,12 @@ namespace vs {
 #ifndef VS_X_WL  // DOFs per thread and step of the LIGHT stream pass (1 or 2)
 #define VS_X_WL 2
 #endif
+#ifndef VS_X_LU  // light stream pass: 2 = two pair-steps per loop trip, all loads first
+#define VS_X_LU 2
+#endif
+#ifndef VS_X_NT2  // threads of a block that take part in the stream passes of HBM-sized operators
+#define VS_X_NT2 768
+#endif
 #ifndef VS_X_BPF2  // stream pass: L2 prefetch by the copy engine too (measured slower there: P2 182 -> 195 us)
 #define VS_X_BPF2 0
 #endif
@@ -116,8 +122,6 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
     const uint16_t *cidx = G.cidx;
     const uint64_t *rec = G.rec;
     const int2 *xb = G.xb;
-    const uint4 *esc = G.esc;
-    __builtin_assume(__isGlobal(esc));
     const bool halo = G.zpeer[0] != nullptr;
     __builtin_assume(__isGlobal(x));
     __builtin_assume(__isGlobal(sv));
@@ -134,6 +138,12 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
     const uint32_t pf1 = (((P.dbg >> 4) & 15u) ? ((P.dbg >> 4) & 15u) : 2u * P.pf_dist) * stride;
     const uint32_t pfd_l = (((P.dbg >> 8) & 15u) ? ((P.dbg >> 8) & 15u) : P.pf_dist) * stride;
     const uint32_t pfd_h = (((P.dbg >> 12) & 15u) ? ((P.dbg >> 12) & 15u) : P.pf_dist) * stride;
+
+    // Threads of a block that take part in the stream passes.  With all 1024 streaming from HBM the
+    // SMs get unequal shares of the bandwidth and a pass ends 8 % after its mean block (C4 512^3:
+    // P2 160 -> 153 us, the grid sum after it 34 -> 15); operators whose vectors largely stay in L2
+    // want every thread (C2 256^3: P2 13.1 vs 13.9 us).
+    const uint32_t nt2 = (P.m_global > 8.0e6 && VS_X_NT2 < NT) ? VS_X_NT2 : NT;
 
     // first / last owned plane of a slab -> the neighbour slab's ghost plane of ring buffer b
     auto halo_to = [&](int b, int fam, uint32_t i, double zi) {
@@ -154,7 +164,9 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
         if (fx == DX_ESC) {  // escape (periodic wrap in y or z, a distance outside its field)
             const uint64_t eo = d >> SH_EORD;
             if (eo) {  // the gather indices from the escape table: one round trip, no record, no bitmask words
-                const uint4 a = __ldg(esc + 2 * (eo - 1)), b = __ldg(esc + 2 * (eo - 1) + 1);
+                const uint4 *et = G.esc + 2 * (eo - 1);  // (pointer re-read from shared memory: not held in a register)
+                __builtin_assume(__isGlobal(et));
+                const uint4 a = __ldg(et), b = __ldg(et + 1);
                 j[0] = a.x;
                 j[1] = a.y;
                 j[2] = a.z;
@@ -169,7 +181,9 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
                 for (int s = 0; s < NS; ++s) pres |= (rec_has_nb<OP>(rc, s) ? 1u : 0u) << s;
                 return;
             }
-            rc = rec[i];  // the table was full: the record and the bitmask lookups
+            const uint64_t *rp = G.rec;
+            __builtin_assume(__isGlobal(rp));
+            rc = rp[i];  // the table was full: the record and the bitmask lookups
             uint32_t nr[NS];
             neighbour_ranks<DIM, OP>(family_meta<OP>(G, rc), P.nw, P.n, G.nx, rc, i, nr);
             pres = 0;
@@ -203,8 +217,17 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
         }
     };
 
+    // The scalars of the iteration live in shared memory, not in registers: thread 0 writes them
+    // after a grid sum, a block barrier follows, and a pass reads what it needs into locals.  Held
+    // in registers (~40 of the 64) they made ptxas split P1's six gathers into dependent batches.
+    __shared__ struct {
+        double mu, rz, rp0, ru0, beta, alpha_prev, rp_last, sval;
+        long long sat, its;
+        unsigned long long t[4], ph[4];
+        int status, conv;
+    } S;
     // ---- setup (krylov.py:102-119): project rhs; r = op(x0) - rhs; z = M^-1 r; d = 0
-    double mu_rhs = 0.0, mu = 0.0, rz = 0.0, rp0 = 0.0, ru0 = 0.0;
+    double mu_rhs = 0.0;
     if (PROJ) {
         double v[1] = {0.0};
         for (uint32_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], G.rhs[i]);
@@ -244,37 +267,46 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
             v[4] = __dadd_rn(v[4], ri);
         }
         grid_sum_shfl<5, true, NT>(v, 1, P, gen, s_warp, s_tot);
-        if (PROJ) {
-            mu = v[3] / P.m_global;
-            v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
-            v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
+        if (threadIdx.x == 0) {
+            double mu = 0.0;
+            if (PROJ) {
+                mu = v[3] / P.m_global;
+                v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[4]));
+                v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[3]));
+            }
+            S.mu = mu;
+            S.rz = v[0];
+            S.rp0 = S.rp_last = sqrt(v[1]);  // inner solves stop on the preconditioned norm (schur.py:207-210, :259-262)
+            S.ru0 = sqrt(v[2]);
+            S.beta = S.alpha_prev = S.sval = 0.0;
+            S.sat = S.its = 0;
+            S.status = 0;
+            S.conv = (S.rp0 == 0.0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) S.ph[q] = 0;
         }
-        rz = v[0];
-        rp0 = sqrt(v[1]);
-        ru0 = sqrt(v[2]);
+        __syncthreads();
     }
-    const double ref = rp0;  // inner solves stop on the preconditioned norm (schur.py:207-210, :259-262)
-    double beta = 0.0, alpha_prev = 0.0, rp_last = rp0, sval = 0.0;
-    int status = 0;
-    int64_t sat = 0, its = 0;
-    bool conv = (ref == 0.0);
     // pending (d, x) updates: their scalars, oldest first; fbase = ring buffer of the oldest pending z
     // (shared memory: every thread writes the same values, and block barriers of the grid sums
     // lie between a write and the reads -- nothing is carried in registers across P1)
     __shared__ double s_hist[3][PCGX_MAX_DEPTH];
     int pend = 0, fbase = 0, cur = 0;
-    unsigned long long ph[4] = {0, 0, 0, 0};
-    if (!conv) {
+    const bool t0_ = threadIdx.x == 0;
+    if (!S.conv) {
         for (int64_t it = 0; it < P.max_iter; ++it) {
-            if (rz < 0.0) { status = 1; sval = rz; sat = it; break; }
-            if (rz == 0.0) { conv = true; break; }
-            if (P.xgpu && *P.xflag) { status = 4; sat = it; break; }  // a peer rank never arrived
+            {
+                const double rz = S.rz;
+                if (rz < 0.0) { if (t0_) { S.status = 1; S.sval = rz; S.sat = it; } break; }
+                if (rz == 0.0) { if (t0_) S.conv = 1; break; }
+            }
+            if (P.xgpu && *P.xflag) { if (t0_) { S.status = 4; S.sat = it; } break; }  // a peer rank never arrived
             const int nxt = (cur + 1 == M) ? 0 : cur + 1;
             const double *zc_ = G.zr[cur];
             double *zn_ = G.zr[nxt];
             __builtin_assume(__isGlobal(zc_));
             __builtin_assume(__isGlobal(zn_));
-            const uint64_t t0 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
+            if (P.phase_ns && t0_) S.t[0] = gtimer();
             // ---- P1: s = M A z + beta s_old; sums z.Az (, sum Az)
             constexpr int K1 = PROJ ? 2 : 1;
             double v1[K1];
@@ -282,6 +314,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
             for (int s = 0; s < K1; ++s) v1[s] = 0.0;
             auto pass1 = [&](auto first_c) {
                 constexpr bool first = decltype(first_c)::value;
+                const double beta = first ? 0.0 : S.beta;
                 uint64_t dn_ = 0;  // the next step's descriptor and chunk base, carried across the step
                 int2 cbn_ = make_int2(0, 0);
                 if (tid < m) {
@@ -340,13 +373,16 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
                 pass1(std::true_type{});
             else
                 pass1(std::false_type{});
-            const uint64_t t1 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
+            if (P.phase_ns && t0_) S.t[1] = gtimer();
             grid_sum<K1, false, NT>(v1, 2, P, gen, s_val, s_tot);
-            const uint64_t t2 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
-            const double delta = PROJ ? __dsub_rn(v1[0], __dmul_rn(mu, v1[PROJ ? 1 : 0])) : v1[0];
-            const double dq = it == 0 ? delta : __dsub_rn(delta, __dmul_rn(beta, rz) / alpha_prev);
-            if (dq <= 0.0) { status = 2; sval = dq; sat = it; break; }
-            const double alpha = rz / dq, nalpha = -alpha;
+            if (P.phase_ns && t0_) S.t[2] = gtimer();
+            double nalpha;
+            {
+                const double delta = PROJ ? __dsub_rn(v1[0], __dmul_rn(S.mu, v1[PROJ ? 1 : 0])) : v1[0];
+                const double dq = it == 0 ? delta : __dsub_rn(delta, __dmul_rn(S.beta, S.rz) / S.alpha_prev);
+                if (dq <= 0.0) { if (t0_) { S.status = 2; S.sval = dq; S.sat = it; } break; }
+                nalpha = -(S.rz / dq);
+            }
             // ---- P2: z_next = z - alpha s; sums r.z = sum diag z^2, z.z (+ sum z, sum r);
             // heavy (every M-th): d and x brought up to date from the ring
             constexpr int KL = PROJ ? 4 : 2;
@@ -362,9 +398,82 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
                     zo_[q] = G.zr[b >= M ? b - M : b];
                     __builtin_assume(__isGlobal(zo_[q]));
                 }
+                // (every pass ends in a grid barrier, so the passes need not agree on who owns a DOF)
+                if (!heavy && VS_X_LU == 2) {
+                    // the light pass, two pair-steps per trip: thread t owns DOFs 2t, 2t+1 of the
+                    // 2*NT chunks at i and i + 2 stride; all four 16-B loads are issued before the
+                    // first use (26 B per DOF need twice the bytes in flight of one pair-step to
+                    // stream at the heavy pass's rate)
+                    // (only the block's first NT2 threads stream: with all 1024 the SMs get unequal
+                    // shares of the bandwidth and the pass ends 8 % after its mean block)
+                    const uint32_t NT2 = nt2;
+                    if (threadIdx.x >= NT2) return;
+                    const uint32_t tid = (blockIdx.x % P.bpg) * NT2 + threadIdx.x, stride = P.bpg * NT2;
+                    const uint32_t sw = 2 * stride, pfw = 2 * (pfd_l / NT) * NT2;
+                    auto cix = [&](uint32_t i) -> uint32_t {
+                        return i + 1 < m ? *reinterpret_cast<const uint32_t *>(cidx + i) : (i < m ? (uint32_t)cidx[i] : 0u);
+                    };
+                    auto ldp = [&](const double *p, uint32_t i) {
+                        return i + 1 < m ? *reinterpret_cast<const double2 *>(p + i)
+                                         : make_double2(i < m ? p[i] : 0.0, 0.0);
+                    };
+                    uint32_t ca_ = cix(2 * tid), cb_ = cix(2 * tid + sw);  // the next trip's code indices, carried
+                    for (uint32_t i = 2 * tid; i < m; i += 2 * sw) {
+                        const uint32_t ib = i + sw;
+                        if (pfw) {
+                            if (i + 2 * pfw < m) {
+                                prefetch_l2(zc_ + i + 2 * pfw);
+                                prefetch_l2(sv + i + 2 * pfw);
+                            }
+                            if (ib + 2 * pfw < m) {
+                                prefetch_l2(zc_ + ib + 2 * pfw);
+                                prefetch_l2(sv + ib + 2 * pfw);
+                            }
+                        }
+                        const uint32_t cc[2] = {ca_, cb_};
+                        double dgv[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint32_t ci = (e & 1) ? (cc[e >> 1] >> 16) : (cc[e >> 1] & 0xFFFFu);
+                            dgv[e] = __ldg(ctab + (OP == 0 ? (ci & 0xFFu) : ci)).y;
+                        }
+                        ca_ = cix(i + 2 * sw);
+                        cb_ = cix(ib + 2 * sw);
+                        const double2 za = ldp(zc_, i), sa = ldp(sv, i), zb = ldp(zc_, ib), sb = ldp(sv, ib);
+                        const double zo[4] = {za.x, za.y, zb.x, zb.y}, si[4] = {sa.x, sa.y, sb.x, sb.y};
+                        double zi[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) zi[e] = xfma<FU>(nalpha, si[e], zo[e]);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint32_t ih = h ? ib : i;
+                            if (ih + 1 < m)
+                                *reinterpret_cast<double2 *>(zn_ + ih) = make_double2(zi[2 * h], zi[2 * h + 1]);
+                            else if (ih < m)
+                                zn_[ih] = zi[2 * h];
+                            if (halo) {
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const uint32_t ci = e ? (cc[h] >> 16) : (cc[h] & 0xFFFFu);
+                                    if (ih + e < m) halo_to(nxt, OP == 0 ? (int)(ci >> 8) : 0, ih + e, zi[2 * h + e]);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {  // a missing DOF contributes zeros
+                            const double ri = __dmul_rn(dgv[e], zi[e]);
+                            v[0] = xfma<FD>(ri, zi[e], v[0]);
+                            v[1] = xfma<FD>(zi[e], zi[e], v[1]);
+                            if (PROJ) {
+                                v[2] = __dadd_rn(v[2], zi[e]);
+                                v[3] = __dadd_rn(v[3], ri);
+                            }
+                        }
+                    }
+                    return;
+                }
                 // the stream pass: thread t of a block step owns W consecutive DOFs of the step's
                 // W*NT chunk (W = 2: 16-B loads and stores)
-                // (every pass ends in a grid barrier, so the passes need not agree on who owns a DOF)
                 constexpr int W = heavy ? VS_X_W : VS_X_WL;
                 static_assert(W == 1 || W == 2, "stream-pass width");
                 auto ldw = [&](const double *p, uint32_t i, bool two, double (&o)[W]) {
@@ -387,7 +496,12 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
                     return (W == 2 && i + 1 < m) ? *reinterpret_cast<const uint32_t *>(cidx + i)
                                                  : (uint32_t)__ldcs(cidx + i);
                 };
-                const uint32_t i0 = W * tid, sw = W * stride, pfw = W * (heavy ? pfd_h : pfd_l);
+                const double beta_h = S.beta, mu_h = S.mu;  // (heavy)
+                const uint32_t NTH = nt2;  // threads that take part (see the light pass)
+                if (threadIdx.x >= NTH) return;
+                const uint32_t tid = (blockIdx.x % P.bpg) * NTH + threadIdx.x, stride = P.bpg * NTH;
+                const uint32_t blk0 = (blockIdx.x % P.bpg) * NTH;
+                const uint32_t i0 = W * tid, sw = W * stride, pfw = W * ((heavy ? pfd_h : pfd_l) / NT) * NTH;
                 uint32_t cin_ = i0 < m ? ldc(i0) : 0u;  // the next step's code indices, carried
                 // this warp's prefetch stream (BPF): z, s, code indices; heavy: d, x, the older z
                 constexpr bool BPF2 = VS_X_BPF2 != 0;
@@ -462,7 +576,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
                                 dd[e] = xfma<FU>(s_hist[1][q], dd[e], PROJ ? __dsub_rn(zh[q][e], s_hist[0][q]) : zh[q][e]);
                                 xx[e] = xfma<FU>(s_hist[2][q], dd[e], xx[e]);
                             }
-                            dd[e] = xfma<FU>(beta, dd[e], PROJ ? __dsub_rn(zo[e], mu) : zo[e]);
+                            dd[e] = xfma<FU>(beta_h, dd[e], PROJ ? __dsub_rn(zo[e], mu_h) : zo[e]);
                             xx[e] = xfma<FU>(nalpha, dd[e], xx[e]);
                         }
                         stw(dv, i, two, dd);
@@ -476,37 +590,51 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
             } else {
                 pass2(std::false_type{});
                 if (pend == 0) fbase = cur;
-                s_hist[0][pend] = mu;
-                s_hist[1][pend] = beta;
-                s_hist[2][pend] = nalpha;
+                if (t0_) {  // (read only after the next grid sum's block barriers)
+                    s_hist[0][pend] = S.mu;
+                    s_hist[1][pend] = S.beta;
+                    s_hist[2][pend] = nalpha;
+                }
                 ++pend;
             }
-            const uint64_t t3 = (P.phase_ns && threadIdx.x == 0) ? gtimer() : 0;
+            if (P.phase_ns && t0_) S.t[3] = gtimer();
             grid_sum<KL, true, NT>(v, 3, P, gen, s_val, s_tot);
-            if (P.phase_ns && threadIdx.x == 0) {
+            if (P.phase_ns && t0_) {
                 const uint64_t t4 = gtimer();
-                ph[0] += t1 - t0;
-                ph[1] += t2 - t1;
-                ph[2] += t3 - t2;
-                ph[3] += t4 - t3;
+                S.ph[0] += S.t[1] - S.t[0];
+                S.ph[1] += S.t[2] - S.t[1];
+                S.ph[2] += S.t[3] - S.t[2];
+                S.ph[3] += t4 - S.t[3];
             }
+            double mu_n = 0.0;
             if (PROJ) {
-                mu = v[2] / P.m_global;
-                v[0] = __dsub_rn(v[0], __dmul_rn(mu, v[3]));
-                v[1] = __dsub_rn(v[1], __dmul_rn(mu, v[2]));
+                mu_n = v[2] / P.m_global;
+                v[0] = __dsub_rn(v[0], __dmul_rn(mu_n, v[3]));
+                v[1] = __dsub_rn(v[1], __dmul_rn(mu_n, v[2]));
             }
-            const double rz_new = v[0];
-            beta = rz_new / rz;
-            rz = rz_new;
-            alpha_prev = alpha;
             cur = nxt;
             const double nz = sqrt(v[1]);
-            if (!isfinite(nz)) { status = 3; sat = it + 1; break; }
-            its = it + 1;
-            rp_last = nz;
-            if (nz / ref < P.tol) { conv = true; break; }
+            const bool bad = !isfinite(nz), done = !bad && nz / S.rp0 < P.tol;
+            // (the old scalars were last read before this grid sum's block barriers; rp0 never changes)
+            if (t0_) {
+                if (bad) {
+                    S.status = 3;
+                    S.sat = it + 1;
+                } else {
+                    S.mu = mu_n;
+                    S.beta = v[0] / S.rz;
+                    S.rz = v[0];
+                    S.alpha_prev = -nalpha;
+                    S.its = it + 1;
+                    S.rp_last = nz;
+                    if (done) S.conv = 1;
+                }
+            }
+            __syncthreads();
+            if (bad || done) break;
         }
     }
+    __syncthreads();  // thread 0's status words of a break before the loop's last barrier
     // ---- the pending (d, x) updates, oldest first (each thread reads only what it wrote)
     if (M > 1 && pend > 0) {
         for (uint32_t i0 = VS_X_W * tid; i0 < m; i0 += VS_X_W * stride) {  // P2's mapping
@@ -532,38 +660,42 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
     if (P.phase_ns && threadIdx.x == 0) {  // [0..3] block 0, [4..7] max, [8..11] sum over blocks
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            if (blockIdx.x == 0) P.phase_ns[p] += ph[p];
-            atomicMax(P.phase_ns + 4 + p, ph[p]);
-            atomicAdd(P.phase_ns + 8 + p, ph[p]);
+            if (blockIdx.x == 0) P.phase_ns[p] += S.ph[p];
+            atomicMax(P.phase_ns + 4 + p, S.ph[p]);
+            atomicAdd(P.phase_ns + 8 + p, S.ph[p]);
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *P.bar_base = gen;  // the next launch on this stream starts from here
         CgOut *o = P.out;
-        o->iterations = its;
-        o->converged = conv ? 1 : 0;
-        o->status = status;
-        o->value = sval;
-        o->at_iter = sat;
-        o->res_prec0 = rp0;
-        o->res_unprec0 = ru0;
-        o->res_prec_last = rp_last;
-        o->res_unprec_last = ru0;
+        o->iterations = S.its;
+        o->converged = S.conv ? 1 : 0;
+        o->status = S.status;
+        o->value = S.sval;
+        o->at_iter = S.sat;
+        o->res_prec0 = S.rp0;
+        o->res_unprec0 = S.ru0;
+        o->res_prec_last = S.rp_last;
+        o->res_unprec_last = S.ru0;
     }
 }
 
-template <int DIM, int OP>
-static const void *pcgx_fn_t(int depth) {
+template <int DIM, int OP, int NT>
+static const void *pcgx_fn_n(int depth) {
     switch (depth) {
-        case 1: return (const void *)k_pcgx<DIM, OP, 1, CG_THREADS>;
-        case 3: return (const void *)k_pcgx<DIM, OP, 3, CG_THREADS>;
-        case 4: return (const void *)k_pcgx<DIM, OP, 4, CG_THREADS>;
-        default: return (const void *)k_pcgx<DIM, OP, 2, CG_THREADS>;
+        case 1: return (const void *)k_pcgx<DIM, OP, 1, NT>;
+        case 3: return (const void *)k_pcgx<DIM, OP, 3, NT>;
+        case 4: return (const void *)k_pcgx<DIM, OP, 4, NT>;
+        default: return (const void *)k_pcgx<DIM, OP, 2, NT>;
     }
 }
-static const void *pcgx_fn(int dim, int op, int depth) {
-    if (dim == 3) return op == 0 ? pcgx_fn_t<3, 0>(depth) : pcgx_fn_t<3, 1>(depth);
-    return op == 0 ? pcgx_fn_t<2, 0>(depth) : pcgx_fn_t<2, 1>(depth);
+template <int DIM, int OP>
+static const void *pcgx_fn_t(int depth, int nt) {
+    return nt == 768 ? pcgx_fn_n<DIM, OP, 768>(depth) : pcgx_fn_n<DIM, OP, CG_THREADS>(depth);
+}
+static const void *pcgx_fn(int dim, int op, int depth, int nt) {
+    if (dim == 3) return op == 0 ? pcgx_fn_t<3, 0>(depth, nt) : pcgx_fn_t<3, 1>(depth, nt);
+    return op == 0 ? pcgx_fn_t<2, 0>(depth, nt) : pcgx_fn_t<2, 1>(depth, nt);
 }
 
 // Plan: one block per SM (per group); no dynamic shared memory.  `unroll` carries the
@@ -577,12 +709,14 @@ CgPlan pcgx_plan(int dim, int op, int64_t m, int groups, int device, int sms) {
     pl.unroll = depth;
     pl.tier = 5;
     pl.threads = CG_THREADS;
+    if (const char *e = getenv("VOXSCHUR_X_THREADS"))  // 768: 24 warps of up to 80 registers
+        if (atoi(e) == 768 || atoi(e) == CG_THREADS) pl.threads = atoi(e);
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     if (sms > 0 && sms < nsm) nsm = sms;
     pl.smem = 0;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcgx_fn(dim, op, depth), pl.threads, pl.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcgx_fn(dim, op, depth, pl.threads), pl.threads, pl.smem);
     if (per_sm < 1) per_sm = 1;
     pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * nsm / groups, (m + pl.threads - 1) / pl.threads));
     pl.slots = 0;
@@ -593,7 +727,7 @@ cudaError_t launch_pcgx(int dim, int op, const CgPlan &pl, int groups, CgParams 
     P.cache_slots = 0;
     P.bpg = pl.grid;
     void *args[] = {&P};
-    return cudaLaunchCooperativeKernel(pcgx_fn(dim, op, pl.unroll), dim3(pl.grid * groups), dim3(pl.threads), args,
+    return cudaLaunchCooperativeKernel(pcgx_fn(dim, op, pl.unroll, pl.threads), dim3(pl.grid * groups), dim3(pl.threads), args,
                                        pl.smem, s);
 }
 

@@ -30,7 +30,7 @@ for _ in range(reps):
     _lib.lib.vs_phase_timing(s._ctx, ph)
     grid = {"A": None}
     print("   phases us/it (P1, sum1, P2, sum2) block0:", np.round(ph[:4] / its / 1e3, 2),
-          "max-block:", np.round(ph[4:8] / its / 1e3, 2))
+          "max-block:", np.round(ph[4:8] / its / 1e3, 2), "mean-block:", np.round(ph[8:12] / its / 1e3 / 148, 2))
     print(f"A-solve [{st['kernel']} u{st['p1_unroll']}]: {its} its, {st['ms']:.3f} ms, {1e3 * st['ms'] / its:.2f} us/it, "
           f"{64 * st['dof_iters'] / st['ms'] / 1e6:.1f} GB/s alg", flush=True)
     z = vx.apply_simple_inverse(s, p, 1e-12)
@@ -38,6 +38,6 @@ for _ in range(reps):
     its = st["iterations"]
     _lib.lib.vs_phase_timing(s._ctx, ph)
     print("   phases us/it (P1, sum1, P2, sum2) block0:", np.round(ph[:4] / its / 1e3, 2),
-          "max-block:", np.round(ph[4:8] / its / 1e3, 2))
+          "max-block:", np.round(ph[4:8] / its / 1e3, 2), "mean-block:", np.round(ph[8:12] / its / 1e3 / 148, 2))
     print(f"S-solve [{st['kernel']} u{st['p1_unroll']}]: {its} its, {st['ms']:.3f} ms, {1e3 * st['ms'] / its:.2f} us/it, "
           f"{64 * st['dof_iters'] / st['ms'] / 1e6:.1f} GB/s alg", flush=True)
