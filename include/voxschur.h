@@ -229,16 +229,19 @@ typedef struct {
                              with q by recurrence, 4 / 5 k_pcgm (M-scaled over 8-B
                              descriptors; s = M q by recurrence / q recomputed), 6 k_pcgb
                              (experimental: S_hat on a blocked order with shared-memory
-                             windows) */
-    int32_t reserved;
+                             windows), 7 k_pcgx (the default at scale: alpha from the z
+                             sums, z in a ring of buffers, d and x updated every M-th
+                             iteration) */
+    int32_t reserved;     /* k_pcgx: the ring depth M; k_pcg<QR>: DOFs per P1 step */
     int32_t tier;         /* where the fused CG took its neighbour ranks from:
                              1 bitmask lookups (records smem-cached), 2 ranks in
                              the smem DOF cache, 3 32-bit ranks streamed from
                              HBM, 4 packed deltas streamed from HBM, 5 8-B
-                             descriptors streamed from HBM (k_pcgm) */
-    int32_t escape_ppm;   /* k_pcgm (tier 5, 8-B descriptors): DOFs per million whose
-                             neighbour deltas do not fit the descriptor and take the
-                             record + bitmask lookup */
+                             descriptors streamed from HBM (k_pcgm, k_pcgx) */
+    int32_t escape_ppm;   /* tier 5 (8-B descriptors): DOFs per million whose neighbour
+                             distances do not fit the descriptor; k_pcgm takes their
+                             ranks from the record + bitmask lookup, k_pcgx from its
+                             escape table */
 } vs_kstat;
 
 int vs_kernel_stats(vs_ctx *ctx, vs_kstat *velocity_cg, vs_kstat *simple_cg,
