@@ -109,7 +109,6 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
     unsigned gen = __ldcg(P.bar_base);
     __syncthreads();
     const Tabs T{s_tab, s_tab + 16, s_tab + 32, P.invS};
-    const double *wS = s_tab + 40;
     const double2 *sdg = P.sdiag2;
     const double2 *ctab = P.ctab;
     __builtin_assume(__isGlobal(ctab));
@@ -351,11 +350,18 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
                         // (The weights are looked up where they are used: loading all six first, or in
                         // pairs, costs registers and ptxas then splits the gathers into more dependent
                         // batches -- P1 205 -> 235 us at C4.)
+                        // (the 3-bit face codes sit at bits 8 + 3f of the record's high word: one
+                        // shift and one mask give the byte offset into the 8-entry weight table)
+                        const uint32_t hi = (uint32_t)(rc >> 32);
+                        auto wgt = [&](int f) {
+                            return *reinterpret_cast<const double *>(reinterpret_cast<const char *>(s_tab) + 40 * 8 +
+                                                                     ((hi >> (5 + 3 * f)) & 0x38u));
+                        };
                         w = 0.0;
 #pragma unroll
                         for (int a = 0; a < DIM; ++a) {
-                            w = xfma<FS>(__dsub_rn(zc, zn[2 * a + 1]), wS[rec_pin(rc, a)], w);
-                            w = xfma<FS>(__dsub_rn(zc, zn[2 * a]), wS[rec_pout(rc, a)], w);
+                            w = xfma<FS>(__dsub_rn(zc, zn[2 * a + 1]), wgt(a), w);      // in face: code a
+                            w = xfma<FS>(__dsub_rn(zc, zn[2 * a]), wgt(3 + a), w);      // out face: code 3 + a
                         }
                     } else {
                         double vn[NS];
@@ -680,22 +686,19 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
     }
 }
 
-template <int DIM, int OP, int NT>
-static const void *pcgx_fn_n(int depth) {
+template <int DIM, int OP>
+static const void *pcgx_fn_t(int depth) {
     switch (depth) {
-        case 1: return (const void *)k_pcgx<DIM, OP, 1, NT>;
-        case 3: return (const void *)k_pcgx<DIM, OP, 3, NT>;
-        case 4: return (const void *)k_pcgx<DIM, OP, 4, NT>;
-        default: return (const void *)k_pcgx<DIM, OP, 2, NT>;
+        case 1: return (const void *)k_pcgx<DIM, OP, 1, CG_THREADS>;
+        case 2: return (const void *)k_pcgx<DIM, OP, 2, CG_THREADS>;
+        case 3: return (const void *)k_pcgx<DIM, OP, 3, CG_THREADS>;
+        default: return (const void *)k_pcgx<DIM, OP, 4, CG_THREADS>;
     }
 }
-template <int DIM, int OP>
-static const void *pcgx_fn_t(int depth, int nt) {
-    return nt == 768 ? pcgx_fn_n<DIM, OP, 768>(depth) : pcgx_fn_n<DIM, OP, CG_THREADS>(depth);
-}
-static const void *pcgx_fn(int dim, int op, int depth, int nt) {
-    if (dim == 3) return op == 0 ? pcgx_fn_t<3, 0>(depth, nt) : pcgx_fn_t<3, 1>(depth, nt);
-    return op == 0 ? pcgx_fn_t<2, 0>(depth, nt) : pcgx_fn_t<2, 1>(depth, nt);
+// (768-thread blocks -- 24 warps of 80 registers -- were measured and lost: C4 S_hat 394.6 vs 392.1 us/it)
+static const void *pcgx_fn(int dim, int op, int depth, int) {
+    if (dim == 3) return op == 0 ? pcgx_fn_t<3, 0>(depth) : pcgx_fn_t<3, 1>(depth);
+    return op == 0 ? pcgx_fn_t<2, 0>(depth) : pcgx_fn_t<2, 1>(depth);
 }
 
 // Plan: one block per SM (per group); no dynamic shared memory.  `unroll` carries the
@@ -709,8 +712,6 @@ CgPlan pcgx_plan(int dim, int op, int64_t m, int groups, int device, int sms) {
     pl.unroll = depth;
     pl.tier = 5;
     pl.threads = CG_THREADS;
-    if (const char *e = getenv("VOXSCHUR_X_THREADS"))  // 768: 24 warps of up to 80 registers
-        if (atoi(e) == 768 || atoi(e) == CG_THREADS) pl.threads = atoi(e);
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     if (sms > 0 && sms < nsm) nsm = sms;

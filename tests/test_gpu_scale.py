@@ -81,8 +81,7 @@ def test_c1_capped_solve_vs_oracle(c1, prec):
                                  {"VOXSCHUR_CG": "5"}, {"VOXSCHUR_CG": "4", "VOXSCHUR_M_THREADS": "512"},
                                  {"VOXSCHUR_CG": "5", "VOXSCHUR_M_THREADS": "512"}, {"VOXSCHUR_TILED": "1"},
                                  {"VOXSCHUR_CG": "7", "VOXSCHUR_X_DEPTH": "1"}, {"VOXSCHUR_CG": "7", "VOXSCHUR_X_DEPTH": "2"},
-                                 {"VOXSCHUR_CG": "7", "VOXSCHUR_X_DEPTH": "3"}, {"VOXSCHUR_CG": "7", "VOXSCHUR_X_DEPTH": "4"},
-                                 {"VOXSCHUR_CG": "7", "VOXSCHUR_X_THREADS": "768"}])
+                                 {"VOXSCHUR_CG": "7", "VOXSCHUR_X_DEPTH": "3"}, {"VOXSCHUR_CG": "7", "VOXSCHUR_X_DEPTH": "4"}])
 def test_c1_other_kernels_vs_oracle(c1, monkeypatch, env):
     """The C1 inner solves with the two-reduction k_pcg (forced) and with the
     experimental TMA-staged plane sweep k_cg1t, against the oracle."""
