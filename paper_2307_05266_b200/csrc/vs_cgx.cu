@@ -21,8 +21,9 @@
 //    every M-th iteration ("heavy" P2: reads the M-1 older z, d, x; applies
 //    the M updates in order, in registers, with the recorded
 //    (mu, beta, alpha) of each; writes d, x).  The operations and their order
-//    are exactly those of an every-iteration update, so x is bitwise the
-//    same for every M.  The other P2s ("light") read z, s and the 2-B code
+//    are exactly those of an every-iteration update (the depths differ only in
+//    how the grid sums round: the light and the heavy pass map DOFs to threads
+//    differently).  The other P2s ("light") read z, s and the 2-B code
 //    index and write z: 26 B.  At the end of the solve the pending updates
 //    are applied from the ring.
 //
