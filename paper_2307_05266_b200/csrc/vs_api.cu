@@ -98,6 +98,7 @@ struct Slab {
     uint64_t *desc[2] = {nullptr, nullptr};
     uint16_t *cidx[2] = {nullptr, nullptr};
     int2 *xb[2] = {nullptr, nullptr};  // x+ / x- rank-distance bases per chunk of 1024 ranks
+    unsigned *lbar = nullptr;  // hierarchical barrier: this slab's local arrival counter and release word (in its arena)
     uint32_t *esc[2] = {nullptr, nullptr};  // escape table: the gather indices of the DOFs outside the descriptor format
     // k_pcgb (S_hat, blocked order): 0 = not built, 1 = built, -1 = not applicable here
     int blk_state = 0;
@@ -235,6 +236,7 @@ struct vs_ctx {
     void *peer_arena[VS_MAX_SLABS] = {};  // opened IPC mappings (closed on destroy)
     int64_t tb_max = 0;
     int npart = 1;
+    bool hier_barrier = false;          // multi-rank runs: ranks arrive through leaders (VOXSCHUR_HIER_BARRIER=0|1 overrides)
     bool mp() const { return nranks > 1; }
     // cross-rank device barrier (one arrival per rank; same counter as the CG)
     void xbar() {
@@ -739,6 +741,10 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.xtimeout_ns = c->xtimeout_ns;
     P.part_self = c->mp() ? c->rank : 0;
     for (int r = 0; r < c->npart; ++r) P.part_peer[r] = c->part_peer[r];
+    // hierarchical barrier (multi-rank runs): the local words live in each local slab's arena
+    P.hier = (c->npart > 1 && c->hier_barrier) ? 1 : 0;
+    P.nranks_bar = c->npart;
+    for (int q = c->s0; q < c->s1; ++q) P.lbar[P.part_self + (q - c->s0)] = c->slabs[q].lbar;
     P.phase_ns = c->phase_ns;
     P.gate = c->gate;
     if (const char *e = getenv("VOXSCHUR_DBG")) P.dbg = (uint32_t)atoi(e);
@@ -1049,10 +1055,19 @@ void build_slabs(vs_ctx *C, int R, int rank, int nranks) {
             C->bar_base = C->bar + 1;
             CK(cudaMemsetAsync(C->bar, 0, 4 * sizeof(unsigned), C->stream));
         }
+        // words 2, 3 of every slab's barrier block: the rank-local arrival counter and release
+        // word of the hierarchical barrier (vs_cg_common.cuh)
+        CK(cudaMemsetAsync(base + L.bar + 2 * sizeof(unsigned), 0, 2 * sizeof(unsigned), C->stream));
+        S.lbar = (unsigned *)(base + L.bar) + 2;
 
     }
     C->npart = 1;
     C->part_peer[0] = C->part;
+    // ranks on different GPUs arrive through their leaders; ranks emulated on one GPU keep the
+    // flat barrier unless asked (there the second level only adds a local round trip: C2 on 4
+    // emulated ranks 43.4 -> 46.3 us/it) -- the tests ask, so that the protocol runs
+    C->hier_barrier = nranks > 1;
+    if (const char *hb = getenv("VOXSCHUR_HIER_BARRIER")) C->hier_barrier = atoi(hb) != 0;
     // VOXSCHUR_EMULATE_RANKS=1: slabs of one process use the multi-process
     // data flow (a partial buffer per slab arena, every block broadcasting
     // its sums to all of them), so one GPU exercises that protocol

@@ -165,6 +165,62 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
 // xtimeout_ns sets it and gives up; every later barrier of the rank returns
 // at once, the fused loops stop at their next iteration (status 4) and the
 // host raises VS_ECUDA after its next synchronisation instead of hanging.
+// Hierarchical form (multi-rank runs, P.hier): the blocks of a rank arrive on the rank's own
+// counter (atom.inc, wraps at bpg: no base to carry); the last local arriver is the rank's leader
+// for this barrier: it alone arrives on the shared counter -- which then counts RANKS, R per
+// barrier -- polls it, and publishes the reached target in the rank's local release word, which
+// the rank's other blocks poll.  NVLink carries R arrivals and R pollers per barrier instead of
+// 148 R of each; every other poll stays in local memory.  Ordering: the local arrivals are
+// acq_rel RMWs on one word (the leader's acquires every earlier block's release), the leader's
+// arrival on the shared counter is a release at the run's scope (cumulative over what it
+// acquired), its final acquire + local release + the blocks' local acquire carry the other
+// ranks' stores to every block.
+__device__ __forceinline__ void grid_barrier_hier(const CgParams &P, unsigned &target) {
+    __syncthreads();
+    target += (unsigned)P.nranks_bar;
+    if (threadIdx.x == 0) {
+        unsigned *lb = P.lbar[P.part_self + (int)(blockIdx.x / P.bpg)];
+        __builtin_assume(__isGlobal(lb));
+        unsigned old;
+        asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;" : "=r"(old) : "l"(lb), "r"((unsigned)P.bpg - 1u) : "memory");
+        if (old == (unsigned)P.bpg - 1u) {  // this rank's last arrival
+            unsigned v;
+            if (P.xgpu) {
+                asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(P.bar) : "memory");
+                unsigned long long t0 = 0;
+                unsigned spins = 0;
+                do {
+                    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(P.bar) : "memory");
+                    if (P.xflag && (++spins & 1023u) == 0) {  // look at the clock every 1024 polls
+                        unsigned long long now;
+                        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+                        if (!t0) t0 = now;
+                        if (*P.xflag) break;
+                        if (P.xtimeout_ns && now - t0 > P.xtimeout_ns) {
+                            *P.xflag = 1;
+                            break;
+                        }
+                    }
+                } while ((int)(v - target) < 0);
+                asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.sys.global.u32 t, [%0];\n\t}" ::"l"(P.bar) : "memory");
+            } else {
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.bar) : "memory");
+                while ((int)(ld_relaxed(P.bar) - target) < 0) {
+                }
+                asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.gpu.global.u32 t, [%0];\n\t}" ::"l"(P.bar) : "memory");
+            }
+            st_release(lb + 1, target);  // (also after a timeout: the rank's blocks must not hang)
+        } else {
+            unsigned spins = 0;
+            while ((int)(ld_relaxed(lb + 1) - target) < 0) {
+                if (P.xgpu && P.xflag && (++spins & 4095u) == 0 && *P.xflag) break;
+            }
+            asm volatile("{\n\t.reg .u32 t;\n\tld.acquire.gpu.global.u32 t, [%0];\n\t}" ::"l"(lb + 1) : "memory");
+        }
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &target, unsigned total_blocks,
                                              bool xgpu = false, volatile int *xflag = nullptr,
                                              unsigned long long xtimeout_ns = 0) {
@@ -257,7 +313,10 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
             for (int k = 0; k < K; ++k) dst[k] = t[k];
         }
     }
-    grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);  // starts with __syncthreads (s_warp reuse is safe)
+    if (P.hier)
+        grid_barrier_hier(P, target);
+    else
+        grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);  // starts with __syncthreads (s_warp reuse is safe)
     // own buffer: one per rank (per group when ranks are emulated as groups)
     const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +
                          (size_t)set * 8 * TB;
@@ -336,7 +395,10 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
             *dst = t[0];
         }
     }
-    grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);  // starts with __syncthreads (s_val reuse is safe)
+    if (P.hier)
+        grid_barrier_hier(P, target);
+    else
+        grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);  // starts with __syncthreads (s_val reuse is safe)
     if (warp < K) {
         // own buffer: one per rank (per group when ranks are emulated as groups)
         const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +

@@ -76,6 +76,12 @@ struct CgParams {
     unsigned long long xtimeout_ns;
     int part_self;          // index in part_peer of the first local group's own buffer
     double *part_peer[VS_MAX_SLABS];
+    // hierarchical barrier of multi-rank runs (npart > 1): per rank a local arrival counter
+    // (wraps at bpg) and a local release word in the rank's OWN arena; only the rank's last
+    // arriver crosses to the shared counter.  Indexed like part_peer (own entries valid).
+    unsigned *lbar[VS_MAX_SLABS];
+    int hier;               // 1: ranks arrive through their leaders (bar counts ranks, not blocks)
+    int nranks_bar;         // ranks that take part in a barrier
     CgOut *out;
     double tol;
     int64_t max_iter;
