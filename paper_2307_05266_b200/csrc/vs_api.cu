@@ -742,7 +742,7 @@ int cg_async(vs_ctx *c, int op, int rhs, int x0, double eps, int x) {
     P.part_self = c->mp() ? c->rank : 0;
     for (int r = 0; r < c->npart; ++r) P.part_peer[r] = c->part_peer[r];
     // hierarchical barrier (multi-rank runs): the local words live in each local slab's arena
-    P.hier = (c->npart > 1 && c->hier_barrier) ? 1 : 0;
+    P.hier = (c->npart > 1 && c->hier_barrier && (op == 0 ? c->plan_A : c->plan_S).alg == CG_TWO_SUM_MX) ? 1 : 0;  // k_pcgx<MR> carries it
     P.nranks_bar = c->npart;
     for (int q = c->s0; q < c->s1; ++q) P.lbar[P.part_self + (q - c->s0)] = c->slabs[q].lbar;
     P.phase_ns = c->phase_ns;

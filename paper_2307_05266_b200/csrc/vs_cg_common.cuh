@@ -165,16 +165,18 @@ __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
 // xtimeout_ns sets it and gives up; every later barrier of the rank returns
 // at once, the fused loops stop at their next iteration (status 4) and the
 // host raises VS_ECUDA after its next synchronisation instead of hanging.
-// Hierarchical form (multi-rank runs, P.hier): the blocks of a rank arrive on the rank's own
-// counter (atom.inc, wraps at bpg: no base to carry); the last local arriver is the rank's leader
-// for this barrier: it alone arrives on the shared counter -- which then counts RANKS, R per
-// barrier -- polls it, and publishes the reached target in the rank's local release word, which
-// the rank's other blocks poll.  NVLink carries R arrivals and R pollers per barrier instead of
-// 148 R of each; every other poll stays in local memory.  Ordering: the local arrivals are
-// acq_rel RMWs on one word (the leader's acquires every earlier block's release), the leader's
-// arrival on the shared counter is a release at the run's scope (cumulative over what it
-// acquired), its final acquire + local release + the blocks' local acquire carry the other
-// ranks' stores to every block.
+// Hierarchical form for multi-rank runs (P.hier; only kernels instantiated with MR = true contain
+// it, so the single-GPU kernels' code is untouched -- at 64 registers they are sensitive to any
+// change around their hot loops: an `if (P.hier)` in the common path cost k_pcgx 3 %).  The blocks
+// of a rank arrive on the rank's own counter (atom.inc, wraps at bpg: no base to carry); the last
+// local arriver is the rank's leader for this barrier: it alone arrives on the shared counter --
+// which then counts RANKS, R per barrier, the unit k_xbar uses -- polls it, and publishes the
+// reached target in the rank's local release word, which the rank's other blocks poll.  NVLink
+// carries R arrivals and R pollers per barrier instead of 148 R of each; every other poll stays in
+// local memory.  Ordering: the local arrivals are acq_rel RMWs on one word (the leader's acquires
+// every earlier block's release), the leader's arrival on the shared counter is a release at the
+// run's scope (cumulative over what it acquired), its final acquire + local release + the blocks'
+// local acquire carry the other ranks' stores to every block.
 __device__ __forceinline__ void grid_barrier_hier(const CgParams &P, unsigned &target) {
     __syncthreads();
     target += (unsigned)P.nranks_bar;
@@ -292,7 +294,7 @@ __device__ __forceinline__ void warp_tree(double (&t)[K]) {
 // the barrier each block reads all blocks' sums from its own buffer in one
 // parallel round trip and reduces them in the same fixed tree, so every
 // block of every rank obtains bitwise-identical totals.
-template <int K, bool ORDER, int NT = CG_THREADS>
+template <int K, bool ORDER, int NT = CG_THREADS, bool MR = false>
 __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgParams &P, unsigned &target,
                                               double (*s_warp)[5], double *s_tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -313,10 +315,14 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
             for (int k = 0; k < K; ++k) dst[k] = t[k];
         }
     }
-    if (P.hier)
-        grid_barrier_hier(P, target);
-    else
-        grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);  // starts with __syncthreads (s_warp reuse is safe)
+    if constexpr (MR) {
+        if (P.hier)
+            grid_barrier_hier(P, target);
+        else
+            grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);
+    } else {
+        grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);
+    }  // starts with __syncthreads (s_warp reuse is safe)
     // own buffer: one per rank (per group when ranks are emulated as groups)
     const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +
                          (size_t)set * 8 * TB;
@@ -354,7 +360,7 @@ __device__ __forceinline__ void grid_sum_shfl(double (&v)[K], int set, const CgP
 // tools/gridsum_variants.cu: K=4 3.93 -> 2.77 us, K=2 2.95 -> 2.52 us per
 // grid sum).  After the barrier warp k again reduces component k over the
 // blocks (lane i: blocks i, i+32, ... in order; loads issued 8 at a time).
-template <int K, bool ORDER, int NT = CG_THREADS>
+template <int K, bool ORDER, int NT = CG_THREADS, bool MR = false>
 __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams &P, unsigned &target,
                                          double (*s_val)[NT], double *s_tot) {
     static_assert(K >= 1 && K <= 8, "grid_sum stages at most 8 components");
@@ -395,10 +401,14 @@ __device__ __forceinline__ void grid_sum(double (&v)[K], int set, const CgParams
             *dst = t[0];
         }
     }
-    if (P.hier)
-        grid_barrier_hier(P, target);
-    else
-        grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);  // starts with __syncthreads (s_val reuse is safe)
+    if constexpr (MR) {
+        if (P.hier)
+            grid_barrier_hier(P, target);
+        else
+            grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);
+    } else {
+        grid_barrier(P.bar, target, TB, P.xgpu, P.xflag, P.xtimeout_ns);
+    }  // starts with __syncthreads (s_val reuse is safe)
     if (warp < K) {
         // own buffer: one per rank (per group when ranks are emulated as groups)
         const double *part = (P.npart > 1 ? P.part_peer[P.part_self + (int)(blockIdx.x / P.bpg)] : P.part) +

@@ -74,7 +74,7 @@ __device__ __forceinline__ double xfma(double a, double b, double c) {
 }
 constexpr int FS = 1, FD = 2, FU = 4;  // stencil, dot products, updates
 
-template <int DIM, int OP, int M, int NT>
+template <int DIM, int OP, int M, int NT, bool MR>
 __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
     if (P.gate && *P.gate) {  // enqueued ahead of the host, and the outer loop is already over
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
     if (PROJ) {
         double v[1] = {0.0};
         for (uint32_t i = tid; i < m; i += stride) v[0] = __dadd_rn(v[0], G.rhs[i]);
-        grid_sum<1, false, NT>(v, 0, P, gen, s_val, s_tot);
+        grid_sum<1, false, NT, MR>(v, 0, P, gen, s_val, s_tot);
         mu_rhs = v[0] / P.m_global;
     }
     {
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
             v[3] = __dadd_rn(v[3], zi);
             v[4] = __dadd_rn(v[4], ri);
         }
-        grid_sum_shfl<5, true, NT>(v, 1, P, gen, s_warp, s_tot);
+        grid_sum_shfl<5, true, NT, MR>(v, 1, P, gen, s_warp, s_tot);
         if (threadIdx.x == 0) {
             double mu = 0.0;
             if (PROJ) {
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
             else
                 pass1(std::false_type{});
             if (P.phase_ns && t0_) S.t[1] = gtimer();
-            grid_sum<K1, false, NT>(v1, 2, P, gen, s_val, s_tot);
+            grid_sum<K1, false, NT, MR>(v1, 2, P, gen, s_val, s_tot);
             if (P.phase_ns && t0_) S.t[2] = gtimer();
             double nalpha;
             {
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
                 ++pend;
             }
             if (P.phase_ns && t0_) S.t[3] = gtimer();
-            grid_sum<KL, true, NT>(v, 3, P, gen, s_val, s_tot);
+            grid_sum<KL, true, NT, MR>(v, 3, P, gen, s_val, s_tot);
             if (P.phase_ns && t0_) {
                 const uint64_t t4 = gtimer();
                 S.ph[0] += S.t[1] - S.t[0];
@@ -687,19 +687,24 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
     }
 }
 
-template <int DIM, int OP>
-static const void *pcgx_fn_t(int depth) {
+template <int DIM, int OP, bool MR>
+static const void *pcgx_fn_m(int depth) {
     switch (depth) {
-        case 1: return (const void *)k_pcgx<DIM, OP, 1, CG_THREADS>;
-        case 2: return (const void *)k_pcgx<DIM, OP, 2, CG_THREADS>;
-        case 3: return (const void *)k_pcgx<DIM, OP, 3, CG_THREADS>;
-        default: return (const void *)k_pcgx<DIM, OP, 4, CG_THREADS>;
+        case 1: return (const void *)k_pcgx<DIM, OP, 1, CG_THREADS, MR>;
+        case 2: return (const void *)k_pcgx<DIM, OP, 2, CG_THREADS, MR>;
+        case 3: return (const void *)k_pcgx<DIM, OP, 3, CG_THREADS, MR>;
+        default: return (const void *)k_pcgx<DIM, OP, 4, CG_THREADS, MR>;
     }
 }
 // (768-thread blocks -- 24 warps of 80 registers -- were measured and lost: C4 S_hat 394.6 vs 392.1 us/it)
-static const void *pcgx_fn(int dim, int op, int depth, int) {
-    if (dim == 3) return op == 0 ? pcgx_fn_t<3, 0>(depth) : pcgx_fn_t<3, 1>(depth);
-    return op == 0 ? pcgx_fn_t<2, 0>(depth) : pcgx_fn_t<2, 1>(depth);
+// mr: the multi-rank instantiation (hierarchical barrier, vs_cg_common.cuh); the single-GPU one does not contain it
+template <int DIM, int OP>
+static const void *pcgx_fn_t(int depth, int mr) {
+    return mr ? pcgx_fn_m<DIM, OP, true>(depth) : pcgx_fn_m<DIM, OP, false>(depth);
+}
+static const void *pcgx_fn(int dim, int op, int depth, int mr) {
+    if (dim == 3) return op == 0 ? pcgx_fn_t<3, 0>(depth, mr) : pcgx_fn_t<3, 1>(depth, mr);
+    return op == 0 ? pcgx_fn_t<2, 0>(depth, mr) : pcgx_fn_t<2, 1>(depth, mr);
 }
 
 // Plan: one block per SM (per group); no dynamic shared memory.  `unroll` carries the
@@ -718,7 +723,7 @@ CgPlan pcgx_plan(int dim, int op, int64_t m, int groups, int device, int sms) {
     if (sms > 0 && sms < nsm) nsm = sms;
     pl.smem = 0;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcgx_fn(dim, op, depth, pl.threads), pl.threads, pl.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcgx_fn(dim, op, depth, 0), pl.threads, pl.smem);
     if (per_sm < 1) per_sm = 1;
     pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * nsm / groups, (m + pl.threads - 1) / pl.threads));
     pl.slots = 0;
@@ -729,7 +734,7 @@ cudaError_t launch_pcgx(int dim, int op, const CgPlan &pl, int groups, CgParams 
     P.cache_slots = 0;
     P.bpg = pl.grid;
     void *args[] = {&P};
-    return cudaLaunchCooperativeKernel(pcgx_fn(dim, op, pl.unroll, pl.threads), dim3(pl.grid * groups), dim3(pl.threads), args,
+    return cudaLaunchCooperativeKernel(pcgx_fn(dim, op, pl.unroll, P.hier), dim3(pl.grid * groups), dim3(pl.threads), args,
                                        pl.smem, s);
 }
 
