@@ -60,6 +60,9 @@ namespace vs {
 #ifndef VS_X_NT2  // threads of a block that take part in the stream passes of HBM-sized operators
 #define VS_X_NT2 768
 #endif
+#ifndef VS_X_U2  // stencil pass: two steps per loop trip (carried words ping-ponged)
+#define VS_X_U2 1
+#endif
 #ifndef VS_X_BPF2  // stream pass: L2 prefetch by the copy engine too (measured slower there: P2 182 -> 195 us)
 #define VS_X_BPF2 0
 #endif
@@ -315,21 +318,14 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
             auto pass1 = [&](auto first_c) {
                 constexpr bool first = decltype(first_c)::value;
                 const double beta = first ? 0.0 : S.beta;
-                uint64_t dn_ = 0;  // the next step's descriptor and chunk base, carried across the step
-                int2 cbn_ = make_int2(0, 0);
-                if (tid < m) {
-                    dn_ = __ldcs(desc + tid);
-                    cbn_ = __ldg(xb + (tid >> CHUNK_SHIFT));
-                }
-                uint32_t c0 = blk0;
-                for (uint32_t i = tid; i < m; i += stride, c0 += stride) {
+                // one step: DOF i of the block's chunk c0, its descriptor d and chunk base cb already in
+                // registers; the next step's are loaded into (dn_, cbn_) first -- a whole step to arrive
+                auto step = [&](uint32_t i, uint32_t c0, const uint64_t d, const int2 cb, uint64_t &dn_, int2 &cbn_) {
                     // L2 prefetch of the block's chunk pf1 strides ahead: z, descriptors, s_old
                     if (pf1 && lane == 0 && warp < 3)
                         bulk_pf(c0 + pf1, NT, warp == 0 ? (const void *)zc_ : warp == 1 ? (const void *)desc
                                               : first ? nullptr : (const void *)sv, 3);
-                    const uint64_t d = dn_;
-                    const int2 cb = cbn_;
-                    if (i + stride < m) {  // issued first: a whole step to arrive
+                    if (i + stride < m) {  // issued first
                         dn_ = __ldcs(desc + i + stride);
                         cbn_ = __ldg(xb + ((i + stride) >> CHUNK_SHIFT));
                     }
@@ -374,6 +370,26 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
                     sv[i] = first ? mw : xfma<FU>(beta, so, mw);
                     v1[0] = xfma<FD>(zc, w, v1[0]);
                     if (PROJ) v1[1] = __dadd_rn(v1[1], w);
+                };
+                // two steps per trip, the carried words ping-ponged between two register sets (no moves)
+                uint64_t da = 0, db = 0;
+                int2 ca = make_int2(0, 0), cb2 = ca;
+                if (tid < m) {
+                    da = __ldcs(desc + tid);
+                    ca = __ldg(xb + (tid >> CHUNK_SHIFT));
+                }
+                uint32_t c0 = blk0;
+                for (uint32_t i = tid; i < m; i += stride, c0 += stride) {
+                    step(i, c0, da, ca, db, cb2);
+                    if (VS_X_U2) {
+                        i += stride;
+                        c0 += stride;
+                        if (i >= m) break;
+                        step(i, c0, db, cb2, da, ca);
+                    } else {
+                        da = db;
+                        ca = cb2;
+                    }
                 }
             };
             if (it == 0)
