@@ -137,8 +137,9 @@ __global__ void __launch_bounds__(NT, 1) k_pcgx(const CgParams P) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // L2 prefetch distances in grid strides, per pass (experiment overrides in VOXSCHUR_DBG:
     // bits 4-7 P1, 8-11 light P2, 12-15 heavy P2)
-    // (P1 looks twice as far ahead: C4 S_hat P1 232 -> 218, A 463 -> 402 us)
-    const uint32_t pf1 = (((P.dbg >> 4) & 15u) ? ((P.dbg >> 4) & 15u) : 2u * P.pf_dist) * stride;
+    // (P1 looks three strides ahead: against one, C4 S_hat P1 232 -> 218, A 463 -> 402 us; three
+    // against two, same call: S_hat 389.8 -> 389.2, A 784.6 -> 780.0 us/it)
+    const uint32_t pf1 = (((P.dbg >> 4) & 15u) ? ((P.dbg >> 4) & 15u) : 3u * P.pf_dist) * stride;
     const uint32_t pfd_l = (((P.dbg >> 8) & 15u) ? ((P.dbg >> 8) & 15u) : P.pf_dist) * stride;
     const uint32_t pfd_h = (((P.dbg >> 12) & 15u) ? ((P.dbg >> 12) & 15u) : P.pf_dist) * stride;
 
